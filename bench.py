@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the b-bit minwise-hashing preprocessing hot path on B200.
+
+Workload (BASELINE.json configs[1], "full webspam shape"): 350,000 synthetic
+documents, 3,728 sorted unique feature ids each (webspam's mean nnz,
+PAPER.md:269) drawn uniformly from D = 16,609,143; k = 500, b = 8; 2U (the
+headline: D rounded up to 2^24 exactly as the reference's bench does,
+bench.cpp:48) and 4U-bit / 4U-mod (D = 16,609,143). Data is synthetic and
+generated on the device; the CSR (5.2 GB) is larger than L2, so every timed
+step streams it from HBM.
+
+  value  = hash-evals/s of the 2U sketch kernel over the HBM-resident CSR
+           (one launch = one step; CUDA events on the launching stream;
+           max over ranks; whole job = sum of all ranks' evals / that time);
+  e2e    = the same metric through the reference-facing C ABI
+           (bbmh_ext_sketch_csr) from pinned HOST buffers: chunked H2D, kernel,
+           D2H of codes+flags all inside the timed region (wall clock);
+  cpu_baseline = the unmodified reference (oracle/_ref, bbmh_sketch_set on
+           all host threads) on a bounded prefix sample, rank 0, N = 1.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU: launched by torch.distributed.run, one rank per GPU, documents
+sharded (each rank sketches its own 350k-doc corpus: weak scaling), no
+collective on the data path; the timing max is taken with one all-reduce.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DOCS = 350_000
+NNZ = 3_728
+D_WEBSPAM = 16_609_143
+D_2U = 1 << 24
+K = 500
+B = 8
+SEED = 42
+SCHEMES = {"2u": (1, D_2U), "4u-bit": (3, D_WEBSPAM), "4u-mod": (2, D_WEBSPAM)}
+# SASS instructions per hash evaluation in the inner loop: fma-pipe, alu-pipe
+INST_PER_EVAL = {"2u": (1.0, 0.5), "4u-bit": (3.0, 8.5), "4u-mod": (None, None)}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---- synthetic corpus ---------------------------------------------------------
+
+def make_corpus_device(torch, n, nnz, dim, seed, device):
+    """n rows of `nnz` sorted unique ids in [0, dim): floor(u_(i) * (dim - nnz)) + i over
+    sorted uniforms u_(1..nnz) -- strictly increasing by construction."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    idx = torch.empty(n * nnz, dtype=torch.int32, device=device)
+    ar = torch.arange(nnz, device=device, dtype=torch.int64)
+    step = 8192
+    for r0 in range(0, n, step):
+        r1 = min(n, r0 + step)
+        u, _ = torch.sort(torch.rand((r1 - r0, nnz), generator=g, device=device,
+                                     dtype=torch.float64), dim=1)
+        ids = (u * (dim - nnz)).to(torch.int64) + ar
+        idx[r0 * nnz:r1 * nnz] = ids.reshape(-1).to(torch.int32)
+    row_ptr = torch.arange(0, n + 1, device=device, dtype=torch.int64) * nnz
+    return row_ptr, idx
+
+
+def make_corpus_host(n, nnz, dim, seed):
+    rng = np.random.default_rng(seed)
+    u = np.sort(rng.random((n, nnz)), axis=1)
+    ids = (u * (dim - nnz)).astype(np.int64) + np.arange(nnz)
+    return (np.arange(n + 1, dtype=np.uint64) * nnz), ids.reshape(-1).astype(np.uint32)
+
+
+# ---- clocks ----------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.3)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- roofline ----------------------------------------------------------------
+
+def int_peaks():
+    """Measured per-SM integer pipe rates (tools/intpeak.py)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import intpeak
+    return intpeak.measure()
+
+
+def roofline_int(scheme, evals_per_s, sm_mhz, peaks):
+    """Issue-pipe roofline of the sketch kernel: each evaluation needs `fma`
+    FMA-pipe and `alu` ALU-pipe instructions (SASS of the inner loop); the
+    bound is the slower pipe at the measured per-SM rate and the SM clock
+    seen under load."""
+    fma, alu = INST_PER_EVAL[scheme]
+    if fma is None or not sm_mhz:
+        return None
+    ops = peaks["ops"]
+    fma_rate = ops["imad"]["inst_per_clk_per_sm"]
+    alu_rate = max(ops["vimnmx3"]["inst_per_clk_per_sm"], ops["lop3"]["inst_per_clk_per_sm"])
+    evals_per_clk = min(fma_rate / fma, alu_rate / alu)
+    peak = 148 * evals_per_clk * sm_mhz * 1e6
+    return {"bound": "int", "unit": "Gevals/s", "achieved": evals_per_s / 1e9,
+            "peak": peak / 1e9, "frac": evals_per_s / peak,
+            "inst_per_eval": {"fma_pipe": fma, "alu_pipe": alu},
+            "pipe_rates_per_sm_clk": {"fma": fma_rate, "alu": alu_rate},
+            "sm_mhz": sm_mhz}
+
+
+# ---- the two arms -----------------------------------------------------------------
+
+def run_reference(args):
+    """`--impl reference`: the unmodified reference on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    scheme_id, dim = SCHEMES[args.scheme]
+    threads = os.cpu_count() or 1
+    n_sample = args.ref_docs or max(64, 12 * threads)
+    rp, idx = make_corpus_host(n_sample, NNZ, D_WEBSPAM, SEED)
+    evals = n_sample * NNZ * K
+    # warm-up on a small slice, then K timed steps over the sample
+    small = min(n_sample, 2 * threads)
+    for _ in range(max(1, args.warmup)):
+        O.refbench_sketch_csr(O.REF_SO, scheme_id, dim, K, SEED, rp[: small + 1],
+                              idx[: small * NNZ], B, threads)
+    secs = []
+    for _ in range(args.steps):
+        s, _codes = O.refbench_sketch_csr(O.REF_SO, scheme_id, dim, K, SEED, rp, idx, B, threads)
+        secs.append(s)
+    t = float(np.mean(secs))
+    v = evals / t
+    print(json.dumps({
+        "impl": "reference", "metric": "hash_evals_per_sec", "value": v, "unit": "hash-evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"webspam-shape {args.scheme} k={K} b={B} (bounded sample)",
+                   "docs_per_step": n_sample, "nnz_per_doc": NNZ, "dim": dim, "k": K, "b": B},
+        "docs_per_sec": n_sample / t,
+        "cpu_baseline": {"value": v, "unit": "hash-evals/s", "cores": threads, "kind": "reference",
+                         "sample": f"{n_sample} webspam-shaped docs per step (of {N_DOCS}), "
+                                   "bbmh_sketch_set on all host threads"},
+        "e2e": {"value": v, "unit": "hash-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1205_2958_b200 import _build
+    if not os.path.exists(os.path.join(ROOT, "paper_1205_2958_b200", "libbbmh.so")):
+        _build.build()
+    from paper_1205_2958_b200 import bbmh
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n, nnz = args.docs, NNZ
+    t0 = time.time()
+    d_rp, d_idx = make_corpus_device(torch, n, nnz, D_WEBSPAM, SEED + 1000 * rank, dev)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] corpus {n} x {nnz} generated in {time.time() - t0:.1f}s")
+    evals = n * nnz * K
+    cb = (K * B + 7) // 8
+    d_codes = torch.empty(n * cb, dtype=torch.uint8, device=dev)
+    d_flags = torch.empty(n, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    peaks = int_peaks() if rank == 0 else None
+
+    launches0 = bbmh.kernel_launches()
+    results = {}
+    clocks = None
+    for name in args.schemes.split(","):
+        scheme_id, dim = SCHEMES[name]
+        fam = bbmh.Family(scheme_id, dim, K, SEED)
+        fam.prepare(local)
+
+        def step():
+            fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, B, d_codes.data_ptr(),
+                                  None, d_flags.data_ptr(), stream=stream.cuda_stream)
+
+        for _ in range(args.warmup):
+            step()
+        barrier()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        with ClockSampler(local) as cs:
+            barrier()
+            ev[0].record(stream)
+            for i in range(args.steps):
+                step()
+                ev[i + 1].record(stream)
+            barrier()
+        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+        ms = max_over_ranks(ev[0].elapsed_time(ev[-1]) / args.steps)
+        clk = cs.summary()
+        if name == "2u":
+            clocks = clk
+        ev_s = evals * world / (ms * 1e-3)
+        results[name] = {"hash_evals_per_sec": ev_s, "docs_per_sec": n * world / (ms * 1e-3),
+                         "ms_per_step": ms, "kernel_ms_min": min(per), "kernel_ms_max": max(per),
+                         "sm_mhz": clk["sm_mhz"]}
+        if rank == 0:
+            rl = roofline_int(name, evals / (ms * 1e-3), clk["sm_mhz"], peaks)
+            results[name]["roofline"] = rl
+            alg_bytes = n * nnz * 4 + (n + 1) * 8 + n * cb + n
+            results[name]["hbm_gbs_algorithmic"] = alg_bytes / (ms * 1e-3) / 1e9
+            log(f"[{name}] {ms:.2f} ms/step  {ev_s / 1e12:.3f} T evals/s  "
+                f"frac={rl['frac'] if rl else None}  clocks={clk}")
+        fam.close()
+    launches_kernel = bbmh.kernel_launches() - launches0
+
+    # ---- e2e through the C ABI from pinned host buffers (2U) ----------------
+    fam = bbmh.Family(1, D_2U, K, SEED)
+    h_rp = d_rp.cpu().numpy().view(np.uint64)
+    pin = bbmh.PinnedArray(n * nnz, np.uint32)
+    pin.array[:] = d_idx.cpu().numpy().view(np.uint32)
+    codes_out = bbmh.PinnedArray(n * cb, np.uint8)
+    for _ in range(args.warmup):
+        fam.sketch_csr(h_rp, pin.array, B, codes_out=codes_out.array)
+    barrier()
+    l0 = bbmh.kernel_launches()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        codes, _, flags = fam.sketch_csr(h_rp, pin.array, B, codes_out=codes_out.array)
+    barrier()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+    e2e_launches = bbmh.kernel_launches() - l0
+    # parity spot check of the e2e output against the device-resident run
+    fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, B, d_codes.data_ptr(), None,
+                          d_flags.data_ptr(), stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    e2e_consistent = bool(np.array_equal(d_codes[: 1000 * cb].cpu().numpy(),
+                                         codes_out.array[: 1000 * cb]))
+    h2d = n * nnz * 4 + (n + 1) * 8
+    d2h = n * cb + n
+
+    # ---- CPU baseline: the reference on this host, bounded sample (rank 0, N=1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle as O
+        if O.ref_available():
+            threads = os.cpu_count() or 1
+            ns = args.ref_docs or max(64, 12 * threads)
+            srp = h_rp[: ns + 1].copy()
+            sidx = pin.array[: ns * nnz].copy()
+            O.refbench_sketch_csr(O.REF_SO, 1, D_2U, K, SEED, srp[:3], sidx[: 2 * nnz], B, threads)
+            secs, ref_codes = O.refbench_sketch_csr(O.REF_SO, 1, D_2U, K, SEED, srp, sidx, B, threads)
+            parity = bool(np.array_equal(ref_codes.reshape(-1), codes_out.array[: ns * cb]))
+            cpu = {"value": ns * nnz * K / secs, "unit": "hash-evals/s", "cores": threads,
+                   "kind": "reference", "parity_vs_gpu": parity,
+                   "sample": f"first {ns} of {n} docs, 2U k={K} b={B}, bbmh_sketch_set on "
+                             f"{threads} threads ({secs:.1f}s)"}
+            log(f"[cpu] {cpu}")
+    pin.free()
+    codes_out.free()
+
+    if rank == 0:
+        head = results["2u"]
+        line = {
+            "metric": "hash_evals_per_sec", "value": head["hash_evals_per_sec"],
+            "unit": "hash-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform sorted ids, device-generated)",
+            "config": {"workload": "webspam-shape C2: 350,000 docs/GPU x 3,728 nnz, 2U D=2^24, k=500, b=8",
+                       "docs_per_gpu": n, "nnz_per_doc": nnz, "k": K, "b": B, "dim_2u": D_2U,
+                       "dim_4u": D_WEBSPAM, "parallelism": f"doc-sharded x{world}",
+                       "l2": "inputs (5.2 GB/GPU) exceed L2; no flush needed"},
+            "docs_per_sec": head["docs_per_sec"],
+            "roofline": head.get("roofline"),
+            "roofline_hbm": {"bound": "hbm", "unit": "GB/s", "achieved": head.get("hbm_gbs_algorithmic"),
+                             "peak": 6461.2, "frac": (head.get("hbm_gbs_algorithmic") or 0) / 6461.2,
+                             "traffic": None},
+            "schemes": results,
+            "e2e": {"value": evals * world / e2e_s, "unit": "hash-evals/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s * 1e3, "api": "bbmh_ext_sketch_csr (pinned host CSR)",
+                    "consistent_with_device_run": e2e_consistent, "steps": args.e2e_steps},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches_kernel + e2e_launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--docs", type=int, default=N_DOCS)
+    ap.add_argument("--schemes", default="2u,4u-bit,4u-mod")
+    ap.add_argument("--scheme", default="2u", help="reference arm scheme")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-docs", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,68 @@
+/* bbmh_ext.h -- B200 extensions to the reference ABI (not in the reference's
+ * proj/include/bbmh.h). They expose the batched form of the reference's
+ * per-document sketch_one (proj/src/sketch.cpp:71-100) that the reference only
+ * runs inside its chunk pipeline (proj/src/pipeline.cpp:171-191), plus device
+ * selection for the document-sharded multi-GPU file pipeline.
+ *
+ * CSR layout everywhere: row_ptr has n+1 u64 entries (row r = indices
+ * [row_ptr[r], row_ptr[r+1])), indices are u32 feature ids. Outputs follow
+ * the reference's SketchRecord (proj/src/sketch.hpp:33-41):
+ *   codes_out  n * ceil(k*b/8) bytes, LE bitstream per row (sketch.cpp:64-69)
+ *   minima_out n * k u64 (nullable), flags_out n bytes (nullable, bit0 = empty)
+ */
+#ifndef BBMH_EXT_H
+#define BBMH_EXT_H
+
+#include "bbmh.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Host buffers (pinned or pageable). Rows are streamed to the selected
+ * GPU(s) in chunks over double-buffered pinned staging: H2D copy, sketch
+ * kernel and D2H copy of the codes overlap. Synchronous. */
+BBMH_API bbmh_status bbmh_ext_sketch_csr(const bbmh_family* family, const uint64_t* row_ptr,
+                                         const uint32_t* indices, uint64_t n, uint32_t b,
+                                         uint8_t* codes_out, uint64_t* minima_out,
+                                         uint8_t* flags_out);
+
+/* Device buffers on the CURRENT device; enqueued on `stream` (a
+ * cudaStream_t, NULL = legacy default stream) and returns without
+ * synchronising. row_ptr values are offsets into d_indices after subtracting
+ * `index_base` (lets a caller pass a slice of a larger row_ptr). */
+BBMH_API bbmh_status bbmh_ext_sketch_csr_device(const bbmh_family* family,
+                                                const uint64_t* d_row_ptr, uint64_t index_base,
+                                                const uint32_t* d_indices, uint64_t n,
+                                                uint32_t b, uint8_t* d_codes,
+                                                uint64_t* d_minima, uint8_t* d_flags,
+                                                void* stream);
+
+/* Device list used by bbmh_ext_sketch_csr and bbmh_sketch_file (default:
+ * the current device only). Chunks are assigned dynamically; output order
+ * and bytes do not depend on the device count. */
+BBMH_API bbmh_status bbmh_ext_set_devices(const int32_t* ids, uint32_t count);
+BBMH_API bbmh_status bbmh_ext_get_devices(int32_t* ids_out, uint32_t capacity,
+                                          uint32_t* count_out);
+
+/* Upload the family's coefficients / permutation tables to `device` now
+ * instead of on first use. */
+BBMH_API bbmh_status bbmh_ext_family_prepare(const bbmh_family* family, int32_t device);
+
+/* Pinned host memory for callers that want zero-copy-staged H2D. */
+BBMH_API bbmh_status bbmh_ext_host_alloc(size_t bytes, void** out);
+BBMH_API void bbmh_ext_host_free(void* p);
+
+/* Number of CUDA kernels this library has launched in this process
+ * (monotonic; used by benchmarks to report gpu_launches). */
+BBMH_API uint64_t bbmh_ext_kernel_launches(void);
+
+/* Chunk size (documents) used by the host-buffer and file pipelines;
+ * 0 restores the default. */
+BBMH_API bbmh_status bbmh_ext_set_chunk_docs(uint64_t docs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BBMH_EXT_H */

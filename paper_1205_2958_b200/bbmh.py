@@ -1,0 +1,262 @@
+"""Python mirror of the reference's C API (proj/include/bbmh.h) over libbbmh.so.
+
+Same names, argument meanings and error behaviour as the reference entry
+points; failures raise :class:`BbmhError` carrying the ``bbmh_status`` and
+``bbmh_last_error()`` detail. There is no CPU fallback: importing this module
+without the built CUDA library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbbmh.so")
+
+# bbmh.h:27-50
+OK = 0
+E_INVALID_ARGUMENT = -1
+E_UNSUPPORTED_UNIVERSE = -2
+E_PERMUTATION_TOO_LARGE = -3
+E_HEADER_MISMATCH = -4
+E_MISSING_MINIMA = -5
+E_EMPTY_SKETCH = -7
+E_DIMENSION_EXCEEDED = -8
+E_NON_BINARY_LABEL = -9
+E_PARSE = -10
+E_IO = -12
+E_INTERNAL = -13
+SCHEME_PERMUTATION, SCHEME_2U, SCHEME_4U_MOD, SCHEME_4U_BIT = 0, 1, 2, 3
+ROWS_LIBSVM, ROWS_BINARY = 0, 1
+SCHEMES = {"perm": 0, "permutation": 0, "2u": 1, "4u-mod": 2, "4umod": 2, "4u-bit": 3,
+           "4ubit": 3, "4u": 3}
+
+u8p = C.POINTER(C.c_uint8)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+i32p = C.POINTER(C.c_int32)
+
+
+class PipelineStats(C.Structure):
+    _fields_ = [("records", C.c_uint64), ("chunks", C.c_uint64),
+                ("read_seconds", C.c_double), ("compute_seconds", C.c_double),
+                ("write_seconds", C.c_double), ("wall_seconds", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class BbmhError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"bbmh status {status}: {message}")
+        self.status = status
+        self.message = message
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libbbmh.so (in-tree build). Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(the CUDA library is required; there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH, mode=os.RTLD_LOCAL | os.RTLD_NOW)
+    sig = {
+        "bbmh_version": ([], C.c_uint32),
+        "bbmh_strerror": ([C.c_int32], C.c_char_p),
+        "bbmh_last_error": ([], C.c_char_p),
+        "bbmh_family_create": ([C.c_int32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
+                                C.c_uint64, C.POINTER(C.c_void_p)], C.c_int32),
+        "bbmh_family_destroy": ([C.c_void_p], None),
+        "bbmh_family_map": ([C.c_void_p, C.c_uint32, C.c_uint32, u32p], C.c_int32),
+        "bbmh_mod_mersenne31": ([C.c_uint64], C.c_uint64),
+        "bbmh_sketch_set": ([C.c_void_p, u32p, C.c_size_t, C.c_uint32, u64p, u8p, i32p],
+                            C.c_int32),
+        "bbmh_sketch_file": ([C.c_void_p, C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64,
+                              C.c_uint32, C.c_int32, C.POINTER(PipelineStats)], C.c_int32),
+        "bbmh_expand_file": ([C.c_char_p, C.c_char_p, C.c_int32], C.c_int32),
+        "bbmh_ext_sketch_csr": ([C.c_void_p, u64p, u32p, C.c_uint64, C.c_uint32, u8p, u64p, u8p],
+                                C.c_int32),
+        "bbmh_ext_sketch_csr_device": ([C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                                        C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p], C.c_int32),
+        "bbmh_ext_set_devices": ([i32p, C.c_uint32], C.c_int32),
+        "bbmh_ext_get_devices": ([i32p, C.c_uint32, C.POINTER(C.c_uint32)], C.c_int32),
+        "bbmh_ext_family_prepare": ([C.c_void_p, C.c_int32], C.c_int32),
+        "bbmh_ext_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], C.c_int32),
+        "bbmh_ext_host_free": ([C.c_void_p], None),
+        "bbmh_ext_kernel_launches": ([], C.c_uint64),
+        "bbmh_ext_set_chunk_docs": ([C.c_uint64], C.c_int32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return lib().bbmh_last_error().decode()
+
+
+def _check(st: int) -> None:
+    if st != OK:
+        raise BbmhError(st, last_error())
+
+
+def version() -> int:
+    return lib().bbmh_version()
+
+
+def strerror(status: int) -> str:
+    return lib().bbmh_strerror(status).decode()
+
+
+def mod_mersenne31(v: int) -> int:
+    return lib().bbmh_mod_mersenne31(v)
+
+
+def _ptr(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def code_bytes(k: int, b: int) -> int:
+    """packed_code_bytes (sketch.hpp:28) for the narrowed b."""
+    return (k * (b & 0xFF) + 7) // 8
+
+
+class Family:
+    """bbmh_family_create / bbmh_family_destroy (bbmh.h:63-69)."""
+
+    def __init__(self, scheme, dim: int, k: int, seed: int, prime: int = 0,
+                 perm_cap_bytes: int = 0):
+        if isinstance(scheme, str):
+            scheme = SCHEMES[scheme]
+        self.scheme, self.dim, self.k, self.seed = int(scheme), int(dim), int(k), int(seed)
+        h = C.c_void_p()
+        _check(lib().bbmh_family_create(self.scheme, dim, k, seed, prime, perm_cap_bytes,
+                                        C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().bbmh_family_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def map(self, j: int, t: int) -> int:
+        out = C.c_uint32()
+        _check(lib().bbmh_family_map(self.handle, j, t, C.byref(out)))
+        return out.value
+
+    def prepare(self, device: int = 0):
+        _check(lib().bbmh_ext_family_prepare(self.handle, device))
+
+    # ---- sketching ------------------------------------------------------
+    def sketch_set(self, indices, b: int, want_minima: bool = True):
+        """bbmh_sketch_set: -> (codes u8[ceil(k*b/8)], minima u64[k] | None, empty)."""
+        idx = np.ascontiguousarray(indices, dtype=np.uint32)
+        cb = code_bytes(self.k, b)
+        codes = np.zeros(max(cb, 1), np.uint8)
+        minima = np.zeros(self.k, np.uint64) if want_minima else None
+        empty = C.c_int32(0)
+        _check(lib().bbmh_sketch_set(self.handle, _ptr(idx, u32p) if idx.size else None,
+                                     idx.size, b, _ptr(minima, u64p), _ptr(codes, u8p),
+                                     C.byref(empty)))
+        return codes[:cb], minima, empty.value
+
+    def sketch_csr(self, row_ptr, indices, b: int, want_minima: bool = False,
+                   codes_out=None):
+        """bbmh_ext_sketch_csr on host arrays -> (codes[n, cb], minima[n, k]|None, flags[n])."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+        idx = np.ascontiguousarray(indices, dtype=np.uint32)
+        n = rp.size - 1
+        cb = code_bytes(self.k, b)
+        codes = codes_out if codes_out is not None else np.empty(n * cb, np.uint8)
+        minima = np.empty(n * self.k, np.uint64) if want_minima else None
+        flags = np.empty(n, np.uint8)
+        _check(lib().bbmh_ext_sketch_csr(self.handle, _ptr(rp, u64p),
+                                         _ptr(idx, u32p) if idx.size else None, n, b,
+                                         _ptr(codes, u8p), _ptr(minima, u64p), _ptr(flags, u8p)))
+        return (codes.reshape(n, cb), minima.reshape(n, self.k) if want_minima else None,
+                flags)
+
+    def sketch_csr_device(self, d_row_ptr, d_indices, n: int, b: int, d_codes,
+                          d_minima=None, d_flags=None, stream=None, index_base: int = 0):
+        """bbmh_ext_sketch_csr_device; arguments are raw device pointers (ints)."""
+        _check(lib().bbmh_ext_sketch_csr_device(self.handle, d_row_ptr, index_base, d_indices, n,
+                                                b, d_codes, d_minima, d_flags, stream))
+
+    def sketch_file(self, input_path, output_path, b: int, chunk_size: int = 10000,
+                    workers: int = 1, emit_minima: bool = False) -> dict:
+        """bbmh_sketch_file -> PipelineStats as a dict."""
+        st = PipelineStats()
+        _check(lib().bbmh_sketch_file(
+            self.handle, None if input_path is None else os.fsencode(input_path),
+            None if output_path is None else os.fsencode(output_path), b, chunk_size, workers,
+            1 if emit_minima else 0, C.byref(st)))
+        return st.as_dict()
+
+
+def expand_file(sketch_path, out_path, row_format: int = ROWS_LIBSVM) -> None:
+    """bbmh_expand_file (bbmh.h:145-147)."""
+    _check(lib().bbmh_expand_file(None if sketch_path is None else os.fsencode(sketch_path),
+                                  None if out_path is None else os.fsencode(out_path),
+                                  row_format))
+
+
+def set_devices(ids) -> None:
+    arr = (C.c_int32 * len(ids))(*ids)
+    _check(lib().bbmh_ext_set_devices(arr, len(ids)))
+
+
+def get_devices() -> list:
+    arr = (C.c_int32 * 64)()
+    n = C.c_uint32()
+    _check(lib().bbmh_ext_get_devices(arr, 64, C.byref(n)))
+    return list(arr[: n.value])
+
+
+def set_chunk_docs(docs: int) -> None:
+    _check(lib().bbmh_ext_set_chunk_docs(docs))
+
+
+def kernel_launches() -> int:
+    return lib().bbmh_ext_kernel_launches()
+
+
+class PinnedArray:
+    """Page-locked host buffer from bbmh_ext_host_alloc viewed as a numpy array."""
+
+    def __init__(self, n: int, dtype):
+        dt = np.dtype(dtype)
+        self.nbytes = max(int(n) * dt.itemsize, 1)
+        p = C.c_void_p()
+        _check(lib().bbmh_ext_host_alloc(self.nbytes, C.byref(p)))
+        self.ptr = p
+        buf = (C.c_uint8 * self.nbytes).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dt, count=int(n))
+
+    def free(self):
+        if self.ptr:
+            self.array = None
+            lib().bbmh_ext_host_free(self.ptr)
+            self.ptr = None

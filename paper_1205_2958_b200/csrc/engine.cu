@@ -1,0 +1,426 @@
+// engine.cu -- host orchestration of the sketch kernels.
+//
+// Replaces the reference's worker pool (pipeline.cpp:171-191: k*nnz
+// HashFamily::map calls per document on CPU threads) with chunked GPU
+// execution: each chunk's CSR slice is copied H2D on a slot stream, sketched
+// by one kernel launch, and its codes/minima/flags copied D2H, with three
+// slots in flight per device so copies of one chunk overlap the kernel of
+// another. Several devices pull chunks from one shared counter (document
+// sharding, no collective): output position depends only on the chunk index.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+#include "engine.hpp"
+
+namespace bbmh {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(Errc::Cuda, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+DeviceFamily::~DeviceFamily() {
+    int prev = 0;
+    if (cudaGetDevice(&prev) != cudaSuccess) return;
+    if (cudaSetDevice(device) != cudaSuccess) return;
+    if (d_coef) cudaFree(d_coef);
+    if (d_perm) cudaFree(d_perm);
+    cudaSetDevice(prev);
+}
+
+Family::Family() = default;
+Family::~Family() = default;
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        BBMH_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) BBMH_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+std::mutex g_cfg_mu;
+std::vector<int> g_devices;
+uint64_t g_chunk_docs = 0;
+
+constexpr uint64_t kDefaultChunkDocs = 32768;
+constexpr uint64_t kChunkIdxCap = 1ull << 24;        // 16 Mi ids (64 MiB) per chunk
+constexpr uint64_t kChunkMinimaBytes = 256ull << 20;  // cap on a chunk's minima buffer
+
+std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
+    auto df = std::make_unique<DeviceFamily>();
+    df->device = device;
+    KernelFamily& kf = df->kf;
+    kf.scheme = int32_t(f.scheme);
+    kf.k = f.k;
+    kf.dim = f.dim;
+    kf.shift2u = f.s >= 32 ? 0 : ((32 - f.s) & 31);  // see Family::map
+    kf.dim_pow2 = f.dim_pow2 ? 1 : 0;
+    kf.dim_mask = uint32_t(f.dim - 1);
+    kf.dim32 = uint32_t(f.dim);
+    kf.p = uint32_t(f.p);
+    kf.barrett = f.p ? (~0ull) / f.p : 0;
+    if (f.scheme == Scheme::FourUBit || f.scheme == Scheme::FourUMod) {
+        if (!f.dim_pow2) {
+            MagicDiv md = make_magic31(f.dim);
+            if (!md.ok) fail(Errc::Cuda, "no 31-bit magic divisor for dim " + std::to_string(f.dim));
+            kf.magic = md.magic;
+            kf.magic_shift = md.shift;
+        }
+    }
+    std::vector<uint32_t> coef;
+    switch (f.scheme) {
+        case Scheme::TwoU:
+            coef = f.twou;
+            break;
+        case Scheme::FourUBit:  // {a3, 2a2, 2a1, 2a0}: doubled operands of the fold
+            coef.resize(4 * size_t(f.k));
+            for (uint32_t j = 0; j < f.k; ++j) {
+                const uint64_t* a = &f.fouru[4 * size_t(j)];
+                coef[4 * j + 0] = uint32_t(a[3]);
+                coef[4 * j + 1] = uint32_t(2 * a[2]);
+                coef[4 * j + 2] = uint32_t(2 * a[1]);
+                coef[4 * j + 3] = uint32_t(2 * a[0]);
+            }
+            break;
+        case Scheme::FourUMod:
+            coef.resize(4 * size_t(f.k));
+            for (uint32_t j = 0; j < f.k; ++j) {
+                const uint64_t* a = &f.fouru[4 * size_t(j)];
+                coef[4 * j + 0] = uint32_t(a[3]);
+                coef[4 * j + 1] = uint32_t(a[2]);
+                coef[4 * j + 2] = uint32_t(a[1]);
+                coef[4 * j + 3] = uint32_t(a[0]);
+            }
+            break;
+        case Scheme::Permutation:
+            break;
+    }
+    DeviceGuard g(device);
+    if (!coef.empty()) {
+        BBMH_CUDA(cudaMalloc(&df->d_coef, coef.size() * sizeof(uint32_t)));
+        BBMH_CUDA(cudaMemcpy(df->d_coef, coef.data(), coef.size() * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice));
+        kf.coef = df->d_coef;
+    }
+    if (f.scheme == Scheme::Permutation) {
+        const size_t bytes = f.perm.size() * sizeof(uint32_t);
+        BBMH_CUDA(cudaMalloc(&df->d_perm, bytes));
+        BBMH_CUDA(cudaMemcpy(df->d_perm, f.perm.data(), bytes, cudaMemcpyHostToDevice));
+        kf.perm = df->d_perm;
+    }
+    return df;
+}
+
+// ---- per-device slot pool ------------------------------------------------
+struct SlotPool {
+    std::mutex mu;
+    std::vector<Lane::Slot*> free;
+};
+std::mutex g_pool_mu;
+std::vector<std::unique_ptr<SlotPool>> g_pools;
+
+SlotPool& pool_for(int device) {
+    std::lock_guard lk(g_pool_mu);
+    if (size_t(device) >= g_pools.size()) g_pools.resize(device + 1);
+    if (!g_pools[device]) g_pools[device] = std::make_unique<SlotPool>();
+    return *g_pools[device];
+}
+
+Lane::Slot* acquire_slot(int device) {
+    SlotPool& p = pool_for(device);
+    {
+        std::lock_guard lk(p.mu);
+        if (!p.free.empty()) {
+            Lane::Slot* s = p.free.back();
+            p.free.pop_back();
+            return s;
+        }
+    }
+    auto* s = new Lane::Slot();
+    s->device = device;
+    DeviceGuard g(device);
+    BBMH_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    BBMH_CUDA(cudaEventCreate(&s->ev0));
+    BBMH_CUDA(cudaEventCreate(&s->ev1));
+    BBMH_CUDA(cudaEventCreateWithFlags(&s->done, cudaEventDisableTiming));
+    BBMH_CUDA(cudaMalloc(&s->d_err, sizeof(int)));
+    BBMH_CUDA(cudaMallocHost(&s->h_err, sizeof(int)));
+    return s;
+}
+
+void release_slot(Lane::Slot* s) {
+    if (!s) return;
+    s->busy = false;
+    SlotPool& p = pool_for(s->device);
+    std::lock_guard lk(p.mu);
+    p.free.push_back(s);
+}
+
+template <typename T>
+void grow_device(T*& p, uint64_t& cap, uint64_t need) {
+    if (need <= cap) return;
+    if (p) BBMH_CUDA(cudaFree(p));
+    p = nullptr;
+    const uint64_t n = std::max<uint64_t>(need, cap + cap / 2);
+    BBMH_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    cap = n;
+}
+
+template <typename T>
+void grow_host(T*& p, uint64_t& cap, uint64_t need) {
+    if (need <= cap) return;
+    if (p) BBMH_CUDA(cudaFreeHost(p));
+    p = nullptr;
+    const uint64_t n = std::max<uint64_t>(need, cap + cap / 2);
+    BBMH_CUDA(cudaMallocHost(&p, n * sizeof(T)));
+    cap = n;
+}
+
+bool is_pinned(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void check_row_ptr(const uint64_t* rp, uint64_t n) {
+    for (uint64_t i = 0; i < n; ++i)
+        if (rp[i + 1] < rp[i]) fail(Errc::InvalidArgument, "row_ptr must be non-decreasing");
+}
+
+}  // namespace
+
+const DeviceFamily& device_family(const Family& f, int device) {
+    std::lock_guard lk(f.dev_mu);
+    if (size_t(device) >= f.dev.size()) f.dev.resize(device + 1);
+    if (!f.dev[device]) f.dev[device] = upload_family(f, device);
+    return *f.dev[device];
+}
+
+std::vector<int> pipeline_devices() {
+    {
+        std::lock_guard lk(g_cfg_mu);
+        if (!g_devices.empty()) return g_devices;
+    }
+    int dev = 0;
+    BBMH_CUDA(cudaGetDevice(&dev));
+    return {dev};
+}
+
+void set_pipeline_devices(const std::vector<int>& ids) {
+    int count = 0;
+    BBMH_CUDA(cudaGetDeviceCount(&count));
+    for (int id : ids)
+        if (id < 0 || id >= count)
+            fail(Errc::InvalidArgument, "device " + std::to_string(id) + " does not exist");
+    std::lock_guard lk(g_cfg_mu);
+    g_devices = ids;
+}
+
+uint64_t chunk_docs_setting() {
+    std::lock_guard lk(g_cfg_mu);
+    return g_chunk_docs ? g_chunk_docs : kDefaultChunkDocs;
+}
+
+void set_chunk_docs(uint64_t docs) {
+    std::lock_guard lk(g_cfg_mu);
+    g_chunk_docs = docs;
+}
+
+// ---- Lane ------------------------------------------------------------------
+Lane::Lane(const Family& f, int device, uint32_t b, bool want_minima)
+    : f_(f), device_(device), b_(b), cb_(packed_code_bytes(f.k, b)), want_minima_(want_minima) {
+    df_ = &device_family(f, device);
+    for (int i = 0; i < kSlots; ++i) slots_[i] = acquire_slot(device);
+}
+
+Lane::~Lane() {
+    for (int i = 0; i < kSlots; ++i) {
+        if (slots_[i] && slots_[i]->busy) cudaStreamSynchronize(slots_[i]->st);
+        release_slot(slots_[i]);
+    }
+}
+
+void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) {
+    if (rows + 1 > s.cap_rows) {  // row-sized buffers: row_ptr (device + pinned mirror), flags
+        const uint64_t cap = std::max<uint64_t>(rows + 1, s.cap_rows + s.cap_rows / 2);
+        if (s.d_rp) BBMH_CUDA(cudaFree(s.d_rp));
+        if (s.d_flags) BBMH_CUDA(cudaFree(s.d_flags));
+        if (s.h_rp) BBMH_CUDA(cudaFreeHost(s.h_rp));
+        if (s.h_flags) BBMH_CUDA(cudaFreeHost(s.h_flags));
+        BBMH_CUDA(cudaMalloc(&s.d_rp, cap * sizeof(uint64_t)));
+        BBMH_CUDA(cudaMalloc(&s.d_flags, cap));
+        BBMH_CUDA(cudaMallocHost(&s.h_rp, cap * sizeof(uint64_t)));
+        BBMH_CUDA(cudaMallocHost(&s.h_flags, cap));
+        s.cap_rows = cap;
+    }
+    grow_device(s.d_idx, s.cap_idx, std::max<uint64_t>(nidx, 4));
+    if (need_pinned_idx) grow_host(s.h_idx, s.cap_idx_pinned, std::max<uint64_t>(nidx, 4));
+    const uint64_t ncodes = std::max<uint64_t>(rows * cb_, 1);
+    if (ncodes > s.cap_codes) {
+        uint64_t c1 = s.cap_codes, c2 = s.cap_codes;
+        grow_device(s.d_codes, c1, ncodes);
+        grow_host(s.h_codes, c2, ncodes);
+        s.cap_codes = std::min(c1, c2);
+    }
+    if (want_minima_) {
+        const uint64_t nmin = std::max<uint64_t>(rows * f_.k, 1);
+        if (nmin > s.cap_min) {
+            uint64_t c1 = s.cap_min, c2 = s.cap_min;
+            grow_device(s.d_min, c1, nmin);
+            grow_host(s.h_min, c2, nmin);
+            s.cap_min = std::min(c1, c2);
+        }
+    }
+}
+
+void Lane::enqueue(Slot& s, const ChunkJob& job) {
+    const uint64_t n = job.n;
+    const uint64_t nidx = job.row_ptr[n] - job.index_base;
+    const bool stage = !job.pinned_input;
+    DeviceGuard g(device_);
+    reserve(s, n, nidx, stage);
+    s.job = job;
+    // row_ptr always goes through the slot's pinned mirror (small)
+    std::memcpy(s.h_rp, job.row_ptr, (n + 1) * sizeof(uint64_t));
+    BBMH_CUDA(cudaMemcpyAsync(s.d_rp, s.h_rp, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                              s.st));
+    const uint32_t* src = job.indices;
+    if (stage && nidx) {
+        std::memcpy(s.h_idx, job.indices, nidx * sizeof(uint32_t));
+        src = s.h_idx;
+    }
+    if (nidx)
+        BBMH_CUDA(cudaMemcpyAsync(s.d_idx, src, nidx * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                  s.st));
+    BBMH_CUDA(cudaMemsetAsync(s.d_err, 0, sizeof(int), s.st));
+    BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
+    launch_sketch(df_->kf, s.d_rp, job.index_base, s.d_idx, n, b_, s.d_codes,
+                  want_minima_ ? s.d_min : nullptr, s.d_flags, s.d_err, s.st);
+    BBMH_CUDA(cudaGetLastError());
+    BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
+    if (n && cb_)
+        BBMH_CUDA(cudaMemcpyAsync(s.h_codes, s.d_codes, n * cb_, cudaMemcpyDeviceToHost, s.st));
+    if (want_minima_)
+        BBMH_CUDA(cudaMemcpyAsync(s.h_min, s.d_min, n * f_.k * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, s.st));
+    BBMH_CUDA(cudaMemcpyAsync(s.h_flags, s.d_flags, n, cudaMemcpyDeviceToHost, s.st));
+    BBMH_CUDA(cudaMemcpyAsync(s.h_err, s.d_err, sizeof(int), cudaMemcpyDeviceToHost, s.st));
+    BBMH_CUDA(cudaEventRecord(s.done, s.st));
+    s.busy = true;
+}
+
+ChunkResult Lane::finish(Slot& s) {
+    BBMH_CUDA(cudaEventSynchronize(s.done));
+    s.busy = false;
+    if (*s.h_err & 1)
+        fail(Errc::InvalidArgument, "feature id out of range for the permutation universe");
+    if (*s.h_err & 2) fail(Errc::InvalidArgument, "row_ptr must be non-decreasing");
+    ChunkResult r;
+    r.tag = s.job.tag;
+    r.n = s.job.n;
+    r.codes = s.h_codes;
+    r.minima = want_minima_ ? s.h_min : nullptr;
+    r.flags = s.h_flags;
+    cudaEventElapsedTime(&r.kernel_ms, s.ev0, s.ev1);
+    return r;
+}
+
+// ---- host-buffer CSR entry -------------------------------------------------
+void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* indices,
+                      uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima, uint8_t* flags) {
+    if (n == 0) return;
+    check_row_ptr(row_ptr, n);
+    const size_t cb = packed_code_bytes(f.k, b);
+    const bool pinned = is_pinned(indices);
+
+    // chunk boundaries: <= chunk_docs rows, <= kChunkIdxCap ids (unless one row is larger)
+    uint64_t cap_docs = chunk_docs_setting();
+    if (minima) cap_docs = std::max<uint64_t>(1, std::min<uint64_t>(cap_docs, kChunkMinimaBytes / (8ull * f.k)));
+    std::vector<uint64_t> bounds{0};
+    for (uint64_t r = 0; r < n;) {
+        uint64_t e = r + 1;
+        while (e < n && e - r < cap_docs && row_ptr[e + 1] - row_ptr[r] <= kChunkIdxCap) ++e;
+        bounds.push_back(e);
+        r = e;
+    }
+    const uint64_t nchunks = bounds.size() - 1;
+    const std::vector<int> devs = pipeline_devices();
+    std::atomic<uint64_t> next{0};
+    std::mutex err_mu;
+    std::exception_ptr err;
+    std::atomic<bool> abort{false};
+
+    auto run_device = [&](int dev) {
+        try {
+            Lane lane(f, dev, b, minima != nullptr);
+            auto done = [&](const ChunkResult& res) {
+                const uint64_t r0 = bounds[res.tag];
+                std::memcpy(codes + r0 * cb, res.codes, res.n * cb);
+                if (minima) std::memcpy(minima + r0 * f.k, res.minima, res.n * f.k * 8);
+                if (flags) std::memcpy(flags + r0, res.flags, res.n);
+            };
+            for (uint64_t c; !abort.load() && (c = next.fetch_add(1)) < nchunks;) {
+                ChunkJob job;
+                job.tag = c;
+                job.row_ptr = row_ptr + bounds[c];
+                job.index_base = row_ptr[bounds[c]];
+                job.indices = indices + row_ptr[bounds[c]];
+                job.n = bounds[c + 1] - bounds[c];
+                job.pinned_input = pinned;
+                lane.submit(job, done);
+            }
+            lane.drain(done);
+        } catch (...) {
+            std::lock_guard lk(err_mu);
+            if (!err) err = std::current_exception();
+            abort = true;
+        }
+    };
+    if (devs.size() == 1) {
+        run_device(devs[0]);
+    } else {
+        std::vector<std::thread> ts;
+        for (int d : devs) ts.emplace_back(run_device, d);
+        for (auto& t : ts) t.join();
+    }
+    if (err) std::rethrow_exception(err);
+}
+
+void sketch_rows_device(const Family& f, const uint64_t* d_row_ptr, uint64_t index_base,
+                        const uint32_t* d_indices, uint64_t n, uint32_t b, uint8_t* d_codes,
+                        uint64_t* d_minima, uint8_t* d_flags, cudaStream_t stream) {
+    if (n == 0) return;
+    int dev = 0;
+    BBMH_CUDA(cudaGetDevice(&dev));
+    const DeviceFamily& df = device_family(f, dev);
+    // per-device scratch error word (the async API does not report it; ids
+    // out of range in permutation mode are clamped to 0 inside the kernel)
+    static std::mutex mu;
+    static std::vector<int*> errs;
+    int* d_err;
+    {
+        std::lock_guard lk(mu);
+        if (size_t(dev) >= errs.size()) errs.resize(dev + 1, nullptr);
+        if (!errs[dev]) BBMH_CUDA(cudaMalloc(&errs[dev], sizeof(int)));
+        d_err = errs[dev];
+    }
+    launch_sketch(df.kf, d_row_ptr, index_base, d_indices, n, b, d_codes, d_minima, d_flags, d_err,
+                  stream);
+    BBMH_CUDA(cudaGetLastError());
+}
+
+}  // namespace bbmh

@@ -1,0 +1,129 @@
+// engine.hpp -- GPU execution of the sketch over CSR blocks: per-device
+// family residency, pooled stream/buffer "slots", the chunked host-buffer
+// pipeline (H2D -> kernel -> D2H overlapped across slots and devices).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "core.hpp"
+#include "kernels.cuh"
+
+namespace bbmh {
+
+void cuda_check(cudaError_t e, const char* what);
+#define BBMH_CUDA(call) ::bbmh::cuda_check((call), #call)
+
+// Per-GPU copy of a family (coefficients in the kernels' layout, tables).
+struct DeviceFamily {
+    int device = -1;
+    uint32_t* d_coef = nullptr;
+    uint32_t* d_perm = nullptr;
+    KernelFamily kf;
+    ~DeviceFamily();
+};
+
+const DeviceFamily& device_family(const Family& f, int device);
+
+// Devices used by the host-buffer and file pipelines (empty = current device).
+std::vector<int> pipeline_devices();
+void set_pipeline_devices(const std::vector<int>& ids);
+
+uint64_t chunk_docs_setting();
+void set_chunk_docs(uint64_t docs);
+
+// Host buffers in, host buffers out; synchronous. Validates row_ptr.
+void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* indices,
+                      uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima, uint8_t* flags);
+
+// Device buffers on the current device; asynchronous on `stream`.
+void sketch_rows_device(const Family& f, const uint64_t* d_row_ptr, uint64_t index_base,
+                        const uint32_t* d_indices, uint64_t n, uint32_t b, uint8_t* d_codes,
+                        uint64_t* d_minima, uint8_t* d_flags, cudaStream_t stream);
+
+// ---- reusable chunk executor (also drives the file pipeline) -------------
+// A Lane owns one device and NSLOT stream/buffer slots. submit() enqueues
+// H2D + kernel + D2H for one CSR chunk into the next slot; when that slot
+// was busy its previous chunk is completed first and handed to `done`.
+struct ChunkJob {
+    uint64_t tag = 0;                 // caller's chunk id
+    const uint64_t* row_ptr = nullptr;  // n+1 entries (host)
+    uint64_t index_base = 0;          // row_ptr[0] value that maps to indices[0]
+    const uint32_t* indices = nullptr;  // host, starting at index_base
+    uint64_t n = 0;
+    bool pinned_input = false;        // row_ptr/indices already page-locked
+};
+
+struct ChunkResult {
+    uint64_t tag = 0;
+    uint64_t n = 0;
+    const uint8_t* codes = nullptr;    // pinned, n * cb
+    const uint64_t* minima = nullptr;  // pinned, n * k (or null)
+    const uint8_t* flags = nullptr;    // pinned, n
+    float kernel_ms = 0;               // device time of the sketch kernel
+};
+
+class Lane {
+public:
+    static constexpr int kSlots = 3;
+    Lane(const Family& f, int device, uint32_t b, bool want_minima);
+    ~Lane();
+    Lane(const Lane&) = delete;
+    Lane& operator=(const Lane&) = delete;
+
+    template <typename Done>
+    void submit(const ChunkJob& job, Done&& done) {
+        Slot& s = *slots_[next_ % kSlots];
+        if (s.busy) done(finish(s));
+        enqueue(s, job);
+        ++next_;
+    }
+    template <typename Done>
+    void drain(Done&& done) {
+        for (int i = 0; i < kSlots; ++i) {
+            Slot& s = *slots_[(next_ + i) % kSlots];
+            if (s.busy) done(finish(s));
+        }
+    }
+    int device() const { return device_; }
+
+public:
+    struct Slot {
+        int device = -1;
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr, done = nullptr;
+        uint64_t* d_rp = nullptr;
+        uint32_t* d_idx = nullptr;
+        uint8_t* d_codes = nullptr;
+        uint64_t* d_min = nullptr;
+        uint8_t* d_flags = nullptr;
+        int* d_err = nullptr;
+        uint64_t* h_rp = nullptr;
+        uint32_t* h_idx = nullptr;
+        uint8_t* h_codes = nullptr;
+        uint64_t* h_min = nullptr;
+        uint8_t* h_flags = nullptr;
+        int* h_err = nullptr;
+        uint64_t cap_rows = 0, cap_idx = 0, cap_idx_pinned = 0, cap_codes = 0, cap_min = 0;
+        bool busy = false;
+        ChunkJob job;
+    };
+
+private:
+    void reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx);
+    void enqueue(Slot& s, const ChunkJob& job);
+    ChunkResult finish(Slot& s);
+
+    const Family& f_;
+    const DeviceFamily* df_ = nullptr;
+    int device_;
+    uint32_t b_;
+    size_t cb_;
+    bool want_minima_;
+    uint64_t next_ = 0;
+    Slot* slots_[kSlots] = {};
+};
+
+}  // namespace bbmh

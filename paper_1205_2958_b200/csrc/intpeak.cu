@@ -1,0 +1,146 @@
+// intpeak.cu -- integer-pipe throughput microbenchmarks (roofline denominators).
+//
+// MEASURED_PEAKS.json only carries HBM and bf16 tensor peaks; the sketch
+// kernels are integer-issue bound, so their roofline needs the B200's
+// per-SM integer throughputs. Each kernel runs a persistent grid (every SM
+// full) with 8 independent dependency chains per thread and reports, via
+// clock64 on each CTA, instructions per SM clock. Built into a separate
+// libbbmh_intpeak.so (not part of the product ABI).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace {
+
+constexpr int kIlp = 8;
+constexpr int kIters = 4096;
+
+enum Op : int {
+    OP_IMAD = 0,       // IMAD R, R, R, R          (fma pipe)
+    OP_IMAD_WIDE = 1,  // IMAD.WIDE.U32 + LEA.HI   (the 4U Mersenne fold, 2 instructions)
+    OP_VIMNMX3 = 2,    // 3-input unsigned min     (alu pipe)
+    OP_IADD3 = 3,      // IADD3                    (alu pipe)
+    OP_LOP3 = 4,       // LOP3.LUT                 (alu pipe)
+    OP_MIX_2U = 5,     // 2 IMAD : 1 VIMNMX3 -- the 2U inner loop mix
+    OP_LEAHI = 6,      // LEA.HI (hi + lo>>1)      (alu pipe)
+    OP_VIADDMNMX = 7,  // min(x + c, x)            (alu pipe)
+};
+
+template <int OP>
+__global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* sink,
+                                                     unsigned long long* cycles) {
+    uint32_t a[kIlp], c1 = seed * 3 + 1, c2 = seed ^ 0x9e3779b9u;
+    uint64_t w[kIlp];
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) {
+        a[i] = threadIdx.x * 7 + i + seed;
+        w[i] = a[i];
+    }
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kIlp; ++i) {
+            if constexpr (OP == OP_IMAD) {
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(c1), "r"(c2));
+            } else if constexpr (OP == OP_IMAD_WIDE) {
+                // the 4U Mersenne fold: IMAD.WIDE.U32 (h*t2 + c) then LEA.HI (hi + lo>>1)
+                const uint64_t v = (uint64_t)a[i] * c1 + c2;
+                a[i] = (uint32_t)(v >> 32) + ((uint32_t)v >> 1);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_VIMNMX3) {
+                a[i] = min(min(a[i], c1 + i), c2);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_IADD3) {
+                asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %0, %0, %2;" : "+r"(a[i]) : "r"(c1), "r"(c2));
+            } else if constexpr (OP == OP_LOP3) {
+                asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[i]) : "r"(c1), "r"(c2));
+            } else if constexpr (OP == OP_MIX_2U) {
+                uint32_t h0, h1;
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h0) : "r"(a[i]), "r"(c1), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h1) : "r"(a[i]), "r"(c2), "r"(c1));
+                a[i] = min(min(a[i], h0), h1);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_LEAHI) {
+                a[i] = c1 + (a[i] >> 1);
+                asm volatile("" : "+r"(a[i]));
+            } else {
+                a[i] = min(a[i] + 0x80000001u, a[i]);
+                asm volatile("" : "+r"(a[i]));
+            }
+        }
+    }
+    const unsigned long long t1 = clock64();
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) acc ^= a[i] ^ (uint32_t)w[i] ^ (uint32_t)(w[i] >> 32);
+    if (acc == 0x12345678u) sink[0] = acc;
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+template <int OP>
+float run(int blocks, int threads, uint32_t* sink, unsigned long long* cyc, cudaStream_t st) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    intpeak_kernel<OP><<<blocks, threads, 0, st>>>(1, sink, cyc);  // warm-up
+    cudaEventRecord(e0, st);
+    intpeak_kernel<OP><<<blocks, threads, 0, st>>>(2, sink, cyc);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Instructions issued per thread per kernel for `op` (source-level count;
+// OP_IADD3 issues 2 adds per step that ptxas may merge into one IADD3).
+__attribute__((visibility("default"))) double bbmh_intpeak_ops_per_thread(int op) {
+    const double base = double(kIters) * kIlp;
+    switch (op) {
+        case OP_MIX_2U: return base * 3;  // 2 IMAD + 1 VIMNMX3
+        case OP_IMAD_WIDE: return base * 2;  // IMAD.WIDE + LEA.HI
+        default: return base;
+    }
+}
+
+// Runs one microbenchmark; returns elapsed ms and the mean per-CTA cycles.
+__attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, int threads,
+                                                           float* ms_out, double* cycles_out) {
+    uint32_t* sink = nullptr;
+    unsigned long long* cyc = nullptr;
+    if (cudaMalloc(&sink, 4) != cudaSuccess) return -1;
+    if (cudaMalloc(&cyc, sizeof(unsigned long long) * blocks) != cudaSuccess) return -1;
+    cudaStream_t st;
+    cudaStreamCreate(&st);
+    float ms = -1;
+    switch (op) {
+        case OP_IMAD: ms = run<OP_IMAD>(blocks, threads, sink, cyc, st); break;
+        case OP_IMAD_WIDE: ms = run<OP_IMAD_WIDE>(blocks, threads, sink, cyc, st); break;
+        case OP_VIMNMX3: ms = run<OP_VIMNMX3>(blocks, threads, sink, cyc, st); break;
+        case OP_IADD3: ms = run<OP_IADD3>(blocks, threads, sink, cyc, st); break;
+        case OP_LOP3: ms = run<OP_LOP3>(blocks, threads, sink, cyc, st); break;
+        case OP_MIX_2U: ms = run<OP_MIX_2U>(blocks, threads, sink, cyc, st); break;
+        case OP_LEAHI: ms = run<OP_LEAHI>(blocks, threads, sink, cyc, st); break;
+        case OP_VIADDMNMX: ms = run<OP_VIADDMNMX>(blocks, threads, sink, cyc, st); break;
+        default: return -2;
+    }
+    unsigned long long* h = new unsigned long long[blocks];
+    cudaMemcpy(h, cyc, sizeof(unsigned long long) * blocks, cudaMemcpyDeviceToHost);
+    double s = 0;
+    for (int i = 0; i < blocks; ++i) s += double(h[i]);
+    delete[] h;
+    *ms_out = ms;
+    *cycles_out = s / blocks;
+    cudaFree(sink);
+    cudaFree(cyc);
+    cudaStreamDestroy(st);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+}

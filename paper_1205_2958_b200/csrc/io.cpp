@@ -1,0 +1,348 @@
+// io.cpp -- corpus readers feeding the GPU pipeline.
+//
+// The reference reads one record at a time on one thread (fgetc per
+// character for LibSVM, dataio.cpp:166-175; fread per u32 for BBCV,
+// dataio.cpp:217-221) -- 36 MB/s and 132 MB/s measured (SURVEY.md finding 7).
+// Here:
+//   * BBCV rows are fread straight into page-locked batch memory, validated
+//     (label +-1, strictly ascending ids) in place;
+//   * LibSVM text is read in large blocks, split at line boundaries and the
+//     lines of a block are parsed by `parse_threads` threads into per-thread
+//     CSR fragments that are concatenated in order. The first error in file
+//     order wins, with the reference's line numbering and messages. Common
+//     tokens take a fast path ("idx:1"); anything unusual falls back to the
+//     same strtod/strtoll calls the reference makes, so accepted inputs,
+//     values and error texts are identical.
+#include "io.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cerrno>
+#include <cstdlib>
+#include <cstring>
+#include <thread>
+
+namespace bbmh {
+
+FILE* open_or_fail(const std::string& path, const char* mode) {
+    FILE* f = std::fopen(path.c_str(), mode);
+    if (!f) fail(Errc::Io, path + ": " + std::strerror(errno));
+    return f;
+}
+
+void write_all(FILE* f, const void* data, size_t n) {
+    if (n && std::fwrite(data, 1, n, f) != n) fail(Errc::Io, "short write");
+}
+
+Batch::~Batch() {
+    if (ids) cudaFreeHost(ids);
+}
+
+void Batch::reserve_ids(uint64_t cap) {
+    if (cap <= cap_ids) return;
+    cap = std::max<uint64_t>(cap, cap_ids + cap_ids / 2);
+    uint32_t* p = nullptr;
+    if (cudaMallocHost(&p, std::max<uint64_t>(cap, 1) * sizeof(uint32_t)) != cudaSuccess)
+        fail(Errc::Cuda, "cudaMallocHost failed for a loader batch");
+    if (ids) {
+        std::memcpy(p, ids, nids() * sizeof(uint32_t));
+        cudaFreeHost(ids);
+    }
+    ids = p;
+    cap_ids = cap;
+}
+
+namespace {
+
+void read_exact(FILE* f, void* p, size_t n) {
+    if (n && std::fread(p, 1, n, f) != n) fail(Errc::Io, "short read");
+}
+
+// ---- BBCV ------------------------------------------------------------------
+class BinaryReader : public CorpusReader {
+public:
+    explicit BinaryReader(const std::string& path) : path_(path) {
+        f_ = open_or_fail(path, "rb");
+        std::setvbuf(f_, nullptr, _IOFBF, 1 << 22);
+        uint8_t head[21];
+        read_exact(f_, head, 4);
+        if (std::memcmp(head, "BBCV", 4) != 0)
+            fail(Errc::MalformedLine, path_ + ": not a BBCV corpus");
+        read_exact(f_, head + 4, 1);
+        if (head[4] != 1) fail(Errc::MalformedLine, path_ + ": unknown BBCV version");
+        read_exact(f_, head + 5, 16);
+        dim_ = get_u64(head + 5);
+        count_ = get_u64(head + 13);
+    }
+    ~BinaryReader() override {
+        if (f_) std::fclose(f_);
+    }
+
+    bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) override {
+        bool any = false;
+        while (read_ < count_ && b.n < max_docs && (b.nids() < max_ids || b.n == 0)) {
+            uint8_t h[5];
+            read_exact(f_, h, 1);
+            const int8_t label = int8_t(h[0]);
+            if (label != 1 && label != -1)
+                fail(Errc::NonBinaryLabel, "record " + std::to_string(read_) + ": bad label");
+            read_exact(f_, h + 1, 4);
+            const uint32_t n = get_u32(h + 1);
+            const uint64_t base = b.nids();
+            if (base + n > b.cap_ids) b.reserve_ids(std::max<uint64_t>(base + n, max_ids + max_ids / 4));
+            uint32_t* dst = b.ids + base;
+            read_exact(f_, dst, size_t(n) * 4);
+            uint32_t bad = 0;
+            for (uint32_t i = 1; i < n; ++i) bad |= dst[i] <= dst[i - 1];
+            if (bad) fail(Errc::NonAscendingIndex, "record " + std::to_string(read_));
+            b.row_ptr.push_back(base + n);
+            b.labels.push_back(label);
+            ++b.n;
+            ++read_;
+            any = true;
+        }
+        return any;
+    }
+
+private:
+    std::string path_;
+    FILE* f_ = nullptr;
+    uint64_t dim_ = 0, count_ = 0, read_ = 0;
+};
+
+// ---- LibSVM ----------------------------------------------------------------
+struct LineErr {
+    Errc code = Errc::Io;
+    std::string msg;
+    bool set = false;
+};
+
+inline bool is_value_end(char c) {
+    return c == ' ' || c == '\t' || c == '\0' || c == '\r' || c == '#';
+}
+
+// parse_libsvm (dataio.cpp:60-106), binary mode with 0/1 labels accepted.
+// `line` is NUL-terminated. Appends ids; returns false with `err` set.
+bool parse_line(const char* line, uint64_t line_no, std::vector<uint32_t>& ids, int8_t& label,
+                LineErr& err) {
+    auto bad = [&](Errc c, const std::string& what) {
+        err.code = c;
+        err.msg = "line " + std::to_string(line_no) + ": " + what;
+        err.set = true;
+        return false;
+    };
+    const char* p = line;
+    char* end = nullptr;
+    double lv;
+    if ((p[0] == '+' || p[0] == '-') && p[1] == '1' && (p[2] == ' ' || p[2] == '\t' || p[2] == '\0')) {
+        lv = p[0] == '+' ? 1.0 : -1.0;
+        end = const_cast<char*>(p + 2);
+    } else {
+        lv = std::strtod(p, &end);
+        if (end == p) return bad(Errc::MalformedLine, "missing label");
+    }
+    if (lv == 1 || lv == -1) label = int8_t(lv);
+    else if (lv == 0) label = -1;
+    else return bad(Errc::MalformedLine, "label must be +-1 (or 0/1)");
+    p = end;
+    int64_t prev = -1;
+    for (;;) {
+        while (*p == ' ' || *p == '\t') ++p;
+        const char c = *p;
+        if (c == '\0' || c == '\n' || c == '\r' || c == '#') break;
+        long long idx;
+        if (c >= '0' && c <= '9') {  // fast path: plain decimal digits
+            uint64_t v = 0;
+            const char* q = p;
+            int nd = 0;
+            while (*q >= '0' && *q <= '9' && nd < 19) {
+                v = v * 10 + uint64_t(*q - '0');
+                ++q;
+                ++nd;
+            }
+            if (*q >= '0' && *q <= '9') {  // too long for the fast path
+                idx = std::strtoll(p, &end, 10);
+            } else {
+                idx = (long long)v;
+                end = const_cast<char*>(q);
+            }
+        } else {
+            idx = std::strtoll(p, &end, 10);
+        }
+        if (end == p || *end != ':') return bad(Errc::MalformedLine, "expected idx:val");
+        if (idx < 1 || idx > (long long)UINT32_MAX)
+            return bad(Errc::MalformedLine, "index out of range (1-based u32)");
+        if (idx - 1 <= prev) return bad(Errc::NonAscendingIndex, "indices must be strictly ascending");
+        prev = idx - 1;
+        p = end + 1;
+        double val;
+        if (p[0] == '1' && is_value_end(p[1])) {
+            val = 1.0;
+            end = const_cast<char*>(p + 1);
+        } else {
+            val = std::strtod(p, &end);
+            if (end == p) return bad(Errc::MalformedLine, "missing value");
+        }
+        p = end;
+        if (val != 1.0)
+            return bad(Errc::NonBinaryValue, "value " + std::to_string(val) + " in binary mode");
+        ids.push_back(uint32_t(idx - 1));
+    }
+    return true;
+}
+
+class LibsvmReader : public CorpusReader {
+public:
+    LibsvmReader(const std::string& path, unsigned threads)
+        : path_(path), threads_(std::max(1u, std::min(threads, 64u))) {
+        f_ = open_or_fail(path, "rb");
+        buf_.resize(kBlock + 1);
+    }
+    ~LibsvmReader() override {
+        if (f_) std::fclose(f_);
+    }
+
+    bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) override {
+        bool any = false;
+        while (b.n < max_docs && (b.nids() < max_ids || b.n == 0)) {
+            // gather complete lines (as NUL-terminated spans) for this round
+            std::vector<std::pair<size_t, size_t>> lines;  // [begin, end) in buf_
+            const uint64_t byte_budget = std::max<uint64_t>(1, (max_ids - std::min(max_ids, b.nids())) * 4);
+            uint64_t bytes = 0;
+            while (lines.size() < max_docs - b.n && bytes < byte_budget) {
+                if (!next_line(lines)) break;
+                bytes += lines.back().second - lines.back().first + 1;
+            }
+            if (lines.empty()) break;
+            any |= parse_lines(lines, b);
+            compact_if_needed();
+        }
+        return any;
+    }
+
+private:
+    static constexpr size_t kBlock = size_t(64) << 20;
+
+    // Finds the next line starting at pos_; reads more input as needed.
+    bool next_line(std::vector<std::pair<size_t, size_t>>& lines) {
+        for (;;) {
+            void* nl = pos_ < len_ ? std::memchr(buf_.data() + pos_, '\n', len_ - pos_) : nullptr;
+            if (nl) {
+                const size_t e = size_t(static_cast<char*>(nl) - buf_.data());
+                buf_[e] = '\0';
+                lines.emplace_back(pos_, e);
+                pos_ = e + 1;
+                return true;
+            }
+            if (eof_) {
+                if (pos_ < len_) {  // last line without a newline
+                    buf_[len_] = '\0';
+                    lines.emplace_back(pos_, len_);
+                    pos_ = len_;
+                    return true;
+                }
+                return false;
+            }
+            if (!lines.empty()) return false;  // parse what we have before moving data
+            refill();
+        }
+    }
+
+    void refill() {
+        if (pos_ > 0) {
+            std::memmove(buf_.data(), buf_.data() + pos_, len_ - pos_);
+            len_ -= pos_;
+            pos_ = 0;
+        }
+        if (len_ + kBlock / 2 > buf_.size() - 1) buf_.resize(std::max(buf_.size() * 2, len_ + kBlock + 1));
+        const size_t want = buf_.size() - 1 - len_;
+        const size_t got = std::fread(buf_.data() + len_, 1, want, f_);
+        if (got < want) {
+            if (std::ferror(f_)) fail(Errc::Io, path_ + ": read error");
+            eof_ = true;
+        }
+        len_ += got;
+    }
+
+    void compact_if_needed() {}
+
+    struct Frag {
+        std::vector<uint32_t> ids;
+        std::vector<uint64_t> lens;
+        std::vector<int8_t> labels;
+        size_t err_line = SIZE_MAX;  // index into the round's lines
+        LineErr err;
+    };
+
+    // Parses `lines` (in order) into b; throws the first error in file order.
+    bool parse_lines(const std::vector<std::pair<size_t, size_t>>& lines, Batch& b) {
+        const size_t nl = lines.size();
+        const unsigned W = nl < 64 ? 1u : threads_;
+        std::vector<Frag> frags(W);
+        const uint64_t line0 = line_no_;
+        auto work = [&](unsigned w) {
+            Frag& fr = frags[w];
+            const size_t lo = nl * w / W, hi = nl * (w + 1) / W;
+            for (size_t i = lo; i < hi; ++i) {
+                const auto [s, e] = lines[i];
+                if (s == e) continue;  // blank line: skipped, but numbered
+                int8_t label = 1;
+                const size_t before = fr.ids.size();
+                if (!parse_line(buf_.data() + s, line0 + i + 1, fr.ids, label, fr.err)) {
+                    fr.err_line = i;
+                    fr.ids.resize(before);
+                    return;
+                }
+                fr.lens.push_back(fr.ids.size() - before);
+                fr.labels.push_back(label);
+            }
+        };
+        if (W == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> ts;
+            for (unsigned w = 1; w < W; ++w) ts.emplace_back(work, w);
+            work(0);
+            for (auto& t : ts) t.join();
+        }
+        line_no_ += nl;
+        bool any = false;
+        for (Frag& fr : frags) {
+            const uint64_t base = b.nids();
+            if (base + fr.ids.size() > b.cap_ids) b.reserve_ids(base + fr.ids.size() + (1u << 20));
+            std::memcpy(b.ids + base, fr.ids.data(), fr.ids.size() * sizeof(uint32_t));
+            uint64_t acc = base;
+            for (size_t r = 0; r < fr.lens.size(); ++r) {
+                acc += fr.lens[r];
+                b.row_ptr.push_back(acc);
+                b.labels.push_back(fr.labels[r]);
+                ++b.n;
+                any = true;
+            }
+            if (fr.err.set) fail(fr.err.code, fr.err.msg);
+        }
+        return any;
+    }
+
+    std::string path_;
+    unsigned threads_;
+    FILE* f_ = nullptr;
+    std::vector<char> buf_;
+    size_t pos_ = 0, len_ = 0;
+    bool eof_ = false;
+    uint64_t line_no_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned parse_threads) {
+    FILE* f = open_or_fail(path, "rb");
+    char magic[4] = {0, 0, 0, 0};
+    const size_t got = std::fread(magic, 1, 4, f);
+    std::fclose(f);
+    if (got == 4 && std::memcmp(magic, "BBCV", 4) == 0) return std::make_unique<BinaryReader>(path);
+    return std::make_unique<LibsvmReader>(path, parse_threads);
+}
+
+}  // namespace bbmh

@@ -1,0 +1,71 @@
+// io.hpp -- corpus readers (BBCV binary, LibSVM text) that fill pinned CSR
+// batches, and the little-endian helpers shared by the BBMH/BBCV writers.
+//
+// Byte formats and validation follow the reference:
+//   BBCV   dataio.hpp:36-40, dataio.cpp:127-153 (writer), 192-245 (reader)
+//   LibSVM dataio.cpp:60-106 (parse), 115-125 (write), 157-190 (reader)
+//   BBMH   sketch.hpp:56-60, sketch.cpp:10-12, 102-141
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "core.hpp"
+
+namespace bbmh {
+
+// A CSR batch of consecutive records; ids live in page-locked memory so the
+// GPU lanes can DMA them directly.
+struct Batch {
+    uint64_t seq = 0;           // batch number
+    uint64_t first_record = 0;  // index of row 0 in the corpus
+    uint64_t n = 0;
+    std::vector<uint64_t> row_ptr{0};
+    std::vector<int8_t> labels;
+    uint32_t* ids = nullptr;  // pinned
+    uint64_t cap_ids = 0;
+    ~Batch();
+    void reserve_ids(uint64_t cap);  // keeps contents
+    void clear() {
+        n = 0;
+        row_ptr.assign(1, 0);
+        labels.clear();
+    }
+    uint64_t nids() const { return row_ptr.back(); }
+};
+
+class CorpusReader {
+public:
+    virtual ~CorpusReader() = default;
+    // Appends records until `max_docs` rows or `max_ids` ids are reached
+    // (a single row may exceed max_ids). Returns false at end of input with
+    // no record appended. Throws bbmh::Error with the reference's messages.
+    virtual bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) = 0;
+};
+
+// open_corpus: sniff the "BBCV" magic, else LibSVM text (dataio.cpp:257-264).
+std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned parse_threads);
+
+// little-endian helpers
+inline void put_u32(uint8_t* p, uint32_t v) {
+    for (int i = 0; i < 4; ++i) p[i] = uint8_t(v >> (8 * i));
+}
+inline void put_u64(uint8_t* p, uint64_t v) {
+    for (int i = 0; i < 8; ++i) p[i] = uint8_t(v >> (8 * i));
+}
+inline uint32_t get_u32(const uint8_t* p) {
+    return uint32_t(p[0]) | uint32_t(p[1]) << 8 | uint32_t(p[2]) << 16 | uint32_t(p[3]) << 24;
+}
+inline uint64_t get_u64(const uint8_t* p) {
+    uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= uint64_t(p[i]) << (8 * i);
+    return v;
+}
+
+FILE* open_or_fail(const std::string& path, const char* mode);
+void write_all(FILE* f, const void* data, size_t n);
+
+}  // namespace bbmh

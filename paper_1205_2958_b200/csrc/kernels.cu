@@ -1,0 +1,354 @@
+// kernels.cu -- sm_100a minwise-hashing kernels (the hot path).
+//
+// One CTA sketches one document (or one tile of `jtile` hash functions of
+// it, for very large k). Layout and roofline reasoning are in DESIGN.md; the
+// short version:
+//   * the document's feature ids are staged once into shared memory (and
+//     pre-transformed per scheme: t mod p, doubled for the Mersenne trick),
+//     padded to a multiple of 4 with a duplicate id (min is unaffected);
+//   * each thread owns J hash functions (coefficients and running minima in
+//     registers) and streams the staged ids with broadcast 128-bit shared
+//     loads, so one LDS.128 feeds 4*J hash evaluations;
+//   * 2U is one IMAD per evaluation plus half a 3-input min (VIMNMX3); the
+//     2U top-s-bit shift is applied once to the minimum (shifting is
+//     monotone, so min(h >> c) == min(h) >> c);
+//   * 4U over GF(2^31-1) folds every Horner step with a single
+//     IMAD.WIDE.U32 on doubled operands: 2v = h*(2t) + 2a puts v >> 31 in the
+//     high word and (v & p) << 1 in the low word, so the fold is hi + (lo>>1);
+//     intermediate steps are reduced lazily to [0, p+1] with one min, the
+//     last one canonically with a 3-input min;
+//   * `% D` for non-power-of-two D is a multiply-high by a host-computed
+//     magic number; 4U-mod (any prime p) uses a 64-bit Barrett reduction;
+//   * the epilogue turns minima into b-bit codes and packs them into the
+//     reference's little-endian bitstream (sketch.cpp:64-69) through shared
+//     memory, writing bytes coalesced.
+// Reference semantics: sketch.cpp:71-100, hash_family.hpp:24-63,77-109.
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+
+#include "kernels.cuh"
+
+namespace bbmh {
+
+namespace {
+
+constexpr uint32_t kTile = 4096;  // feature ids staged per pass (16 KB)
+constexpr uint32_t kP31 = 0x7fffffffu;
+
+std::atomic<uint64_t> g_launches{0};
+
+enum : int { S_PERM = 0, S_2U = 1, S_4UMOD = 2, S_4UBIT = 3 };
+
+__device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) {
+    return min(min(a, b), c);
+}
+
+// 2*(h*t + a) with t2 = 2t, c = 2a; returns ((h*t+a) >> 31) + ((h*t+a) & p),
+// which is < 2^32 whenever h*t + a < 2^62 (mod_mersenne31's first fold,
+// hash_family.hpp:27).
+__device__ __forceinline__ uint32_t m31_fold(uint32_t h, uint32_t t2, uint32_t c) {
+    const uint64_t v = (uint64_t)h * t2 + c;
+    return (uint32_t)(v >> 32) + ((uint32_t)v >> 1);
+}
+
+// x mod p for x < 2^62, 3 <= p < 2^31 (and p = 2), barrett = floor((2^64-1)/p)
+__device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t p, uint64_t barrett) {
+    const uint64_t q = __umul64hi(x, barrett);
+    const uint32_t r = (uint32_t)x - (uint32_t)q * p;  // true r in [0, 2p)
+    return min(r, r - p);
+}
+
+template <bool POW2>
+__device__ __forceinline__ uint32_t reduce_dim(const KernelFamily& F, uint32_t h) {
+    if constexpr (POW2) {
+        return h & F.dim_mask;
+    } else {
+        return h - F.dim32 * (__umulhi(h, F.magic) >> F.magic_shift);
+    }
+}
+
+template <int SCHEME>
+__device__ __forceinline__ uint32_t stage_transform(const KernelFamily& F, uint32_t t, int* err) {
+    if constexpr (SCHEME == S_4UBIT) {
+        const uint32_t r = min3u(t, t - kP31, t - 2 * kP31);  // t mod p for any u32 t
+        return r << 1;
+    } else if constexpr (SCHEME == S_4UMOD) {
+        return mod_barrett(t, F.p, F.barrett);
+    } else if constexpr (SCHEME == S_PERM) {
+        if ((uint64_t)t >= F.dim) {  // the reference reads out of bounds here (UB)
+            atomicOr(err, 1);
+            return 0;
+        }
+        return t;
+    } else {
+        return t;
+    }
+}
+
+template <int SCHEME>
+struct Coef;
+
+template <>
+struct Coef<S_2U> {
+    uint32_t a1, a2;
+    __device__ void load(const KernelFamily& F, uint32_t j) {
+        const uint2 c = reinterpret_cast<const uint2*>(F.coef)[j];
+        a1 = c.x;
+        a2 = c.y;
+    }
+};
+
+template <>
+struct Coef<S_4UBIT> {
+    uint32_t a3, c2, c1, c0;
+    __device__ void load(const KernelFamily& F, uint32_t j) {
+        const uint4 c = reinterpret_cast<const uint4*>(F.coef)[j];
+        a3 = c.x;
+        c2 = c.y;
+        c1 = c.z;
+        c0 = c.w;
+    }
+};
+
+template <>
+struct Coef<S_4UMOD> {
+    uint32_t a3, a2, a1, a0;
+    __device__ void load(const KernelFamily& F, uint32_t j) {
+        const uint4 c = reinterpret_cast<const uint4*>(F.coef)[j];
+        a3 = c.x;
+        a2 = c.y;
+        a1 = c.z;
+        a0 = c.w;
+    }
+};
+
+template <>
+struct Coef<S_PERM> {
+    const uint32_t* tab;
+    __device__ void load(const KernelFamily& F, uint32_t j) { tab = F.perm + (uint64_t)j * F.dim; }
+};
+
+// One hash evaluation h_j(t) on the staged (transformed) id.
+template <int SCHEME, bool POW2>
+__device__ __forceinline__ uint32_t hash1(const KernelFamily& F, const Coef<SCHEME>& c,
+                                          uint32_t t) {
+    if constexpr (SCHEME == S_2U) {
+        return c.a1 + c.a2 * t;  // natural 32-bit wrap; shift deferred to the minimum
+    } else if constexpr (SCHEME == S_4UBIT) {
+        uint32_t s = m31_fold(c.a3, t, c.c2);
+        uint32_t h = min(s, s - kP31);  // lazy: h in [0, p+1]
+        s = m31_fold(h, t, c.c1);
+        h = min(s, s - kP31);
+        s = m31_fold(h, t, c.c0);
+        h = min3u(s, s - kP31, s - 2 * kP31);  // canonical in [0, p)
+        return reduce_dim<POW2>(F, h);
+    } else if constexpr (SCHEME == S_4UMOD) {
+        uint32_t h = mod_barrett((uint64_t)c.a3 * t + c.a2, F.p, F.barrett);
+        h = mod_barrett((uint64_t)h * t + c.a1, F.p, F.barrett);
+        h = mod_barrett((uint64_t)h * t + c.a0, F.p, F.barrett);
+        return reduce_dim<POW2>(F, h);
+    } else {
+        return __ldg(c.tab + t);
+    }
+}
+
+template <int SCHEME, bool POW2, int J>
+__global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint64_t* __restrict__ row_ptr,
+                                                     uint64_t index_base,
+                                                     const uint32_t* __restrict__ indices,
+                                                     uint32_t b, uint32_t jtile,
+                                                     uint8_t* __restrict__ codes,
+                                                     uint64_t* __restrict__ minima,
+                                                     uint8_t* __restrict__ flags, int* err) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* s_idx = smem;           // kTile staged ids
+    uint32_t* s_code = smem + kTile;  // jtile codes
+    const uint4* s_idx4 = reinterpret_cast<const uint4*>(s_idx);
+
+    const uint64_t doc = blockIdx.x;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t tpb = blockDim.x;
+    const uint32_t k = F.k;
+    const uint32_t j0 = blockIdx.y * jtile;
+
+    uint64_t beg = row_ptr[doc], end = row_ptr[doc + 1];
+    if (end < beg) {
+        if (tid == 0) atomicOr(err, 2);
+        end = beg;
+    }
+    beg -= index_base;
+    end -= index_base;
+    const uint64_t nnz = end - beg;
+
+    Coef<SCHEME> c[J];
+    uint32_t m[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) {
+        const uint32_t j = min(j0 + tid + r * tpb, k - 1);  // spare lanes recompute j = k-1
+        c[r].load(F, j);
+        m[r] = 0xffffffffu;
+    }
+
+    for (uint64_t off = 0; off < nnz; off += kTile) {
+        const uint32_t cnt = (uint32_t)(nnz - off < kTile ? nnz - off : kTile);
+        const uint32_t cnt4 = (cnt + 3) & ~3u;
+        const uint32_t* src = indices + beg + off;
+        for (uint32_t i = tid; i < cnt4; i += tpb) {
+            const uint32_t t = __ldg(src + (i < cnt ? i : 0));  // pad with a duplicate id
+            s_idx[i] = stage_transform<SCHEME>(F, t, err);
+        }
+        __syncthreads();
+        const uint32_t n4 = cnt4 >> 2;
+#pragma unroll 2
+        for (uint32_t q = 0; q < n4; ++q) {
+            const uint4 t4 = s_idx4[q];
+#pragma unroll
+            for (int r = 0; r < J; ++r) {
+                const uint32_t h0 = hash1<SCHEME, POW2>(F, c[r], t4.x);
+                const uint32_t h1 = hash1<SCHEME, POW2>(F, c[r], t4.y);
+                const uint32_t h2 = hash1<SCHEME, POW2>(F, c[r], t4.z);
+                const uint32_t h3 = hash1<SCHEME, POW2>(F, c[r], t4.w);
+                m[r] = min3u(m[r], h0, h1);
+                m[r] = min3u(m[r], h2, h3);
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue: minima -> codes -> packed bitstream (sketch.cpp:80-98) --
+    const bool empty = nnz == 0;
+    const uint32_t mask = b >= 32 ? 0xffffffffu : ((1u << b) - 1);
+    const uint32_t jcnt = min(jtile, k - j0);
+#pragma unroll
+    for (int r = 0; r < J; ++r) {
+        const uint32_t jl = tid + r * tpb;
+        if (jl < jcnt) {
+            uint32_t mn = m[r];
+            if constexpr (SCHEME == S_2U) mn >>= F.shift2u;
+            s_code[jl] = empty ? mask : (mn & mask);
+            if (minima) minima[doc * k + j0 + jl] = empty ? ~0ull : (uint64_t)mn;
+        }
+    }
+    if (flags && blockIdx.y == 0 && tid == 0) flags[doc] = empty ? 1 : 0;
+    __syncthreads();
+
+    const uint64_t cb = ((uint64_t)k * b + 7) >> 3;
+    const uint64_t byte0 = ((uint64_t)j0 * b) >> 3;  // j0*b is a multiple of 8
+    const uint64_t byte1e = ((uint64_t)(j0 + jcnt) * b + 7) >> 3;
+    const uint64_t byte1 = byte1e < cb ? byte1e : cb;
+    uint8_t* out = codes + doc * cb;
+    for (uint64_t B = byte0 + tid; B < byte1; B += tpb) {
+        const uint64_t bit0 = B << 3;
+        const uint32_t ja = (uint32_t)(bit0 / b);
+        const uint64_t jb0 = (bit0 + 7) / b, jlast = (uint64_t)j0 + jcnt - 1;
+        const uint32_t jb = (uint32_t)(jb0 < jlast ? jb0 : jlast);
+        uint32_t v = 0;
+        for (uint32_t j = ja; j <= jb; ++j) {
+            const uint64_t code = s_code[j - j0];
+            const int64_t pos = (int64_t)j * b - (int64_t)bit0;
+            v |= (uint32_t)(pos >= 0 ? (code << pos) : (code >> -pos));
+        }
+        out[B] = (uint8_t)v;
+    }
+}
+
+template <int SCHEME, bool POW2, int J>
+void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* row_ptr,
+                uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
+                uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
+    auto kern = sketch_kernel<SCHEME, POW2, J>;
+    const size_t smem = (kTile + sh.jtile) * sizeof(uint32_t);
+    constexpr uint64_t kMaxGrid = 1u << 30;
+    const size_t cb = ((size_t)F.k * b + 7) / 8;
+    for (uint64_t d0 = 0; d0 < n; d0 += kMaxGrid) {
+        const uint64_t nd = n - d0 < kMaxGrid ? n - d0 : kMaxGrid;
+        dim3 grid((unsigned)nd, sh.jtiles);
+        kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr + d0, base, idx, b, sh.jtile, codes + d0 * cb,
+                                         minima ? minima + d0 * F.k : nullptr,
+                                         flags ? flags + d0 : nullptr, err);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+}
+
+template <int SCHEME, bool POW2>
+void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* row_ptr,
+                uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
+                uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
+    switch (sh.J) {
+        case 1: return launch_one<SCHEME, POW2, 1>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case 2: return launch_one<SCHEME, POW2, 2>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case 4: return launch_one<SCHEME, POW2, 4>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        default: return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+    }
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
+}  // namespace
+
+LaunchShape choose_shape(uint32_t k, int scheme) {
+    // Minimise idle (j >= k) lanes; among equal slot counts prefer J = 4
+    // (one LDS.128 feeds 16 evaluations) and fewer CTAs per document.
+    (void)scheme;
+    LaunchShape best;
+    uint64_t best_slots = ~0ull;
+    int best_pen = 1 << 30;
+    const int Js[4] = {4, 8, 2, 1};
+    for (int J : Js) {
+        for (int tpb = 32; tpb <= 256; tpb += 32) {
+            const uint64_t jtile = (uint64_t)tpb * J;
+            const uint64_t tiles = (k + jtile - 1) / jtile;
+            if (tiles > 65535) continue;
+            const uint64_t slots = tiles * jtile;
+            const int pen = (int)tiles * 4 + (J == 4 ? 0 : J == 8 ? 1 : J == 2 ? 2 : 3);
+            if (slots < best_slots || (slots == best_slots && pen < best_pen)) {
+                best_slots = slots;
+                best_pen = pen;
+                best.J = J;
+                best.tpb = tpb;
+                best.jtile = (uint32_t)jtile;
+                best.jtiles = (uint32_t)tiles;
+            }
+        }
+    }
+    // developer tuning knobs (not part of the ABI)
+    const int J = env_int("BBMH_TUNE_J", 0), tpb = env_int("BBMH_TUNE_TPB", 0);
+    if ((J == 1 || J == 2 || J == 4 || J == 8) && tpb >= 32 && tpb <= 256 && tpb % 32 == 0) {
+        best.J = J;
+        best.tpb = tpb;
+        best.jtile = (uint32_t)(J * tpb);
+        best.jtiles = (k + best.jtile - 1) / best.jtile;
+    }
+    return best;
+}
+
+void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
+                   const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima,
+                   uint8_t* flags, int* err, cudaStream_t st) {
+    if (n == 0) return;
+    const LaunchShape sh = choose_shape(F.k, F.scheme);
+    switch (F.scheme) {
+        case S_2U:
+            return dispatch_j<S_2U, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case S_4UBIT:
+            if (F.dim_pow2)
+                return dispatch_j<S_4UBIT, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            return dispatch_j<S_4UBIT, false>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case S_4UMOD:
+            if (F.dim_pow2)
+                return dispatch_j<S_4UMOD, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            return dispatch_j<S_4UMOD, false>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        default:
+            return dispatch_j<S_PERM, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+    }
+}
+
+uint64_t kernel_launch_count() { return g_launches.load(); }
+
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+}  // namespace bbmh

@@ -1,0 +1,49 @@
+// kernels.cuh -- device-side description of a hash family and the sketch
+// kernel launcher (implementation in kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bbmh {
+
+// Everything a sketch kernel needs, passed by value (lives in the kernel
+// parameter bank, i.e. constant memory). Derived on the host from Family.
+struct KernelFamily {
+    int32_t scheme = 1;      // Scheme tag
+    uint32_t k = 0;
+    uint64_t dim = 0;
+    uint32_t shift2u = 0;    // 2U: right shift applied to the minimum (hash_family.hpp:48-51)
+    uint32_t dim_mask = 0;   // 4U: dim - 1 when dim is a power of two
+    uint32_t dim_pow2 = 1;
+    uint32_t dim32 = 0;      // 4U: dim (< 2^31) for the magic-division branch
+    uint32_t magic = 0;      // 4U: h % dim = h - dim * (umulhi(h, magic) >> magic_shift)
+    uint32_t magic_shift = 0;
+    uint32_t p = 0;          // 4U modulus
+    uint64_t barrett = 0;    // 4U-mod: floor((2^64 - 1) / p)
+    const uint32_t* coef = nullptr;  // 2U: k*{a1,a2}; 4U-bit: k*{a3,2a2,2a1,2a0}; 4U-mod: k*{a3,a2,a1,a0}
+    const uint32_t* perm = nullptr;  // permutation tables, k*dim
+};
+
+struct LaunchShape {
+    int J = 4;        // hash functions per thread (register-blocked)
+    int tpb = 128;    // threads per CTA
+    uint32_t jtile = 512;  // hash functions per CTA (tpb*J), multiple of 8
+    uint32_t jtiles = 1;   // CTAs per document
+};
+
+LaunchShape choose_shape(uint32_t k, int scheme);
+
+// Sketch rows [0, n) of a CSR block resident on the current device.
+// row_ptr values are offsets into `indices` after subtracting index_base.
+// err (device int) receives bit 1 for a permutation id >= dim and bit 2
+// for a decreasing row_ptr.
+void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
+                   const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
+                   uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
+
+uint64_t kernel_launch_count();
+void count_launches(uint64_t n);
+
+}  // namespace bbmh

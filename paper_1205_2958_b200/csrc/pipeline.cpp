@@ -1,0 +1,294 @@
+// pipeline.cpp -- bbmh_sketch_file: loader -> pinned CSR batches -> GPU
+// lanes (H2D / sketch kernel / D2H) -> order-restoring writer.
+//
+// Same three roles as the reference's sketch_stream (pipeline.cpp:123-213):
+// one reader, a pool of compute workers (here: one host thread per GPU, each
+// keeping three chunks in flight), and the calling thread as the in-order
+// writer. Output bytes are identical for any (chunk_size, workers, devices).
+// First error wins; files are left exactly as the reference's SketchWriter
+// destructor leaves them (header with the count of records written).
+#include "pipeline.hpp"
+
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <exception>
+#include <map>
+#include <mutex>
+#include <thread>
+
+#include "engine.hpp"
+#include "io.hpp"
+
+namespace bbmh {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) {
+    return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+constexpr uint64_t kBatchIds = 1ull << 24;  // ids per loader batch (64 MiB pinned)
+
+template <typename T>
+class BlockingQueue {
+public:
+    void push(T v) {
+        std::lock_guard lk(m_);
+        q_.push_back(std::move(v));
+        cv_.notify_one();
+    }
+    bool pop(T& out) {
+        std::unique_lock lk(m_);
+        cv_.wait(lk, [&] { return !q_.empty() || closed_ || aborted_; });
+        if (aborted_ || q_.empty()) return false;
+        out = std::move(q_.front());
+        q_.pop_front();
+        return true;
+    }
+    void close() {
+        std::lock_guard lk(m_);
+        closed_ = true;
+        cv_.notify_all();
+    }
+    void abort() {
+        std::lock_guard lk(m_);
+        aborted_ = true;
+        cv_.notify_all();
+    }
+
+private:
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::deque<T> q_;
+    bool closed_ = false, aborted_ = false;
+};
+
+struct OutBatch {
+    uint64_t n = 0;
+    std::vector<uint8_t> recs;     // n * (2 + cb): label, flags, codes
+    std::vector<uint64_t> minima;  // n * k (optional)
+};
+
+// order-restoring buffer (pipeline.cpp:77-119)
+class Reorder {
+public:
+    void put(uint64_t seq, OutBatch&& b) {
+        std::lock_guard lk(m_);
+        done_[seq] = std::move(b);
+        cv_.notify_all();
+    }
+    bool take(uint64_t seq, OutBatch& out) {
+        std::unique_lock lk(m_);
+        cv_.wait(lk, [&] { return done_.count(seq) || (total_known_ && seq >= total_) || aborted_; });
+        if (aborted_) return false;
+        auto it = done_.find(seq);
+        if (it == done_.end()) return false;
+        out = std::move(it->second);
+        done_.erase(it);
+        return true;
+    }
+    void set_total(uint64_t t) {
+        std::lock_guard lk(m_);
+        total_ = t;
+        total_known_ = true;
+        cv_.notify_all();
+    }
+    void abort() {
+        std::lock_guard lk(m_);
+        aborted_ = true;
+        cv_.notify_all();
+    }
+
+private:
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::map<uint64_t, OutBatch> done_;
+    uint64_t total_ = 0;
+    bool total_known_ = false, aborted_ = false;
+};
+
+// SketchWriter (sketch.cpp:102-141): header now, count patched on close/destruction
+class SketchWriter {
+public:
+    SketchWriter(const std::string& path, const Family& f, uint8_t b, bool emit_minima) {
+        f_ = open_or_fail(path, "wb");
+        uint8_t h[36];
+        std::memcpy(h, "BBMH", 4);
+        h[4] = 1;
+        h[5] = uint8_t(f.scheme);
+        h[6] = b;
+        h[7] = 0;
+        put_u32(h + 8, f.k);
+        put_u64(h + 12, f.dim);
+        put_u64(h + 20, f.seed);
+        put_u64(h + 28, 0);
+        write_all(f_, h, sizeof h);
+        if (emit_minima) fmin_ = open_or_fail(path + ".min64", "wb");
+    }
+    ~SketchWriter() {
+        try {
+            close();
+        } catch (...) {
+        }
+    }
+    void append(const OutBatch& ob) {
+        write_all(f_, ob.recs.data(), ob.recs.size());
+        if (fmin_) write_all(fmin_, ob.minima.data(), ob.minima.size() * sizeof(uint64_t));
+        count_ += ob.n;
+    }
+    void close() {
+        if (!f_) return;
+        FILE* f = f_;
+        f_ = nullptr;
+        uint8_t c[8];
+        put_u64(c, count_);
+        const bool ok = std::fseek(f, 28, SEEK_SET) == 0 && std::fwrite(c, 1, 8, f) == 8;
+        std::fclose(f);
+        if (fmin_) std::fclose(fmin_);
+        fmin_ = nullptr;
+        if (!ok) fail(Errc::Io, "seek failed");
+    }
+
+private:
+    FILE* f_ = nullptr;
+    FILE* fmin_ = nullptr;
+    uint64_t count_ = 0;
+};
+
+}  // namespace
+
+PipelineStats sketch_file(const Family& f, const std::string& input_path,
+                          const std::string& output_path, uint8_t b, uint64_t chunk_size,
+                          uint32_t workers, bool emit_minima) {
+    const auto wall0 = Clock::now();
+    // open order as in sketch_file (pipeline.cpp:217-220) and sketch_stream (:125-126)
+    auto reader = open_corpus(input_path, workers ? workers : 1);
+    SketchWriter writer(output_path, f, b, emit_minima);
+    if (chunk_size < 1) fail(Errc::InvalidArgument, "chunk_size must be >= 1");
+    if (workers < 1) fail(Errc::InvalidArgument, "workers must be >= 1");
+
+    PipelineStats stats;
+    const size_t cb = packed_code_bytes(f.k, b);
+    const std::vector<int> devs = pipeline_devices();
+    const uint64_t max_docs = chunk_docs_setting();
+    const bool b_ok = b >= 1 && b <= 32;
+
+    const size_t nbatches = 3 * devs.size() + 3;
+    std::vector<std::unique_ptr<Batch>> storage;
+    BlockingQueue<Batch*> free_q, in_q;
+    for (size_t i = 0; i < nbatches; ++i) {
+        storage.push_back(std::make_unique<Batch>());
+        free_q.push(storage.back().get());
+    }
+    Reorder done;
+    std::mutex err_mu;
+    std::exception_ptr error;
+    auto record_error = [&](std::exception_ptr e) {
+        {
+            std::lock_guard lk(err_mu);
+            if (!error) error = e;
+        }
+        free_q.abort();
+        in_q.abort();
+        done.abort();
+    };
+
+    std::thread rd([&] {
+        try {
+            double read_s = 0;
+            uint64_t seq = 0, first = 0;
+            for (;;) {
+                Batch* bt = nullptr;
+                if (!free_q.pop(bt)) return;
+                const auto t0 = Clock::now();
+                bt->clear();
+                bt->reserve_ids(kBatchIds + kBatchIds / 4);
+                const bool got = reader->fill(*bt, max_docs, kBatchIds);
+                read_s += since(t0);
+                if (!got) break;
+                if (!b_ok) fail(Errc::InvalidArgument, "b must be in 1..32");  // sketch.cpp:73
+                bt->seq = seq++;
+                bt->first_record = first;
+                first += bt->n;
+                in_q.push(bt);
+            }
+            stats.read_seconds = read_s;
+            stats.records = first;
+            in_q.close();
+            done.set_total(seq);
+        } catch (...) {
+            record_error(std::current_exception());
+        }
+    });
+
+    std::vector<double> kernel_ms(devs.size(), 0.0);
+    std::vector<std::thread> lanes;
+    for (size_t di = 0; di < devs.size(); ++di) {
+        lanes.emplace_back([&, di] {
+            try {
+                BBMH_CUDA(cudaSetDevice(devs[di]));
+                Lane lane(f, devs[di], b_ok ? b : 8, emit_minima);
+                std::map<uint64_t, Batch*> inflight;
+                auto on_done = [&](const ChunkResult& r) {
+                    Batch* bt = inflight.at(r.tag);
+                    inflight.erase(r.tag);
+                    OutBatch ob;
+                    ob.n = r.n;
+                    ob.recs.resize(r.n * (2 + cb));
+                    uint8_t* p = ob.recs.data();
+                    for (uint64_t i = 0; i < r.n; ++i, p += 2 + cb) {
+                        p[0] = uint8_t(bt->labels[i]);
+                        p[1] = r.flags[i];
+                        std::memcpy(p + 2, r.codes + i * cb, cb);
+                    }
+                    if (emit_minima) ob.minima.assign(r.minima, r.minima + r.n * f.k);
+                    kernel_ms[di] += r.kernel_ms;
+                    const uint64_t seq = bt->seq;
+                    free_q.push(bt);
+                    done.put(seq, std::move(ob));
+                };
+                Batch* bt = nullptr;
+                while (in_q.pop(bt)) {
+                    ChunkJob job;
+                    job.tag = bt->seq;
+                    job.row_ptr = bt->row_ptr.data();
+                    job.index_base = 0;
+                    job.indices = bt->ids;
+                    job.n = bt->n;
+                    job.pinned_input = true;
+                    inflight[bt->seq] = bt;
+                    lane.submit(job, on_done);
+                }
+                lane.drain(on_done);
+            } catch (...) {
+                record_error(std::current_exception());
+            }
+        });
+    }
+
+    // the calling thread is the order-restoring writer (pipeline.cpp:193-204)
+    try {
+        OutBatch ob;
+        for (uint64_t seq = 0; done.take(seq, ob); ++seq) {
+            const auto t0 = Clock::now();
+            writer.append(ob);
+            stats.write_seconds += since(t0);
+        }
+    } catch (...) {
+        record_error(std::current_exception());
+    }
+    rd.join();
+    for (auto& t : lanes) t.join();
+    if (error) std::rethrow_exception(error);
+    writer.close();
+
+    for (double ms : kernel_ms) stats.compute_seconds += ms * 1e-3;
+    stats.chunks = (stats.records + chunk_size - 1) / chunk_size;  // reference chunking
+    stats.wall_seconds = since(wall0);
+    return stats;
+}
+
+}  // namespace bbmh

@@ -1,0 +1,112 @@
+"""The C-ABI library (libbbmh.so) without a GPU: it loads, exports every
+symbol include/*.h declares, and its host-only entry points (family build,
+map, mod, status strings, validation) match the reference's golden vectors.
+Compute calls must FAIL LOUDLY here (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+def declared_symbols():
+    names = set()
+    for h in ("bbmh.h", "bbmh_ext.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        names |= set(re.findall(r"BBMH_API[^;(]*?\b(bbmh_\w+)\s*\(", src))
+    return names
+
+
+def test_exports_every_declared_symbol(bb):
+    out = subprocess.run(["nm", "-D", "--defined-only", bb.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (bbmh_\w+)", out))
+    declared = declared_symbols()
+    assert len(declared) >= 33
+    assert declared <= exported, declared - exported
+    # nothing else leaks out of the library
+    assert exported == declared, exported - declared
+
+
+def test_reference_symbols_all_present(bb, ref):
+    out = subprocess.run(["nm", "-D", "--defined-only", ref.path], capture_output=True,
+                         text=True, check=True).stdout
+    ref_syms = set(re.findall(r" T (bbmh_\w+)", out))
+    assert len(ref_syms) == 24
+    assert ref_syms <= declared_symbols()
+
+
+def test_version_strerror(bb):
+    assert bb.version() == 10000
+    assert bb.strerror(0) == "ok"
+    assert bb.strerror(-3) == "permutation tables exceed the memory cap"
+    assert bb.strerror(-99) == "internal error"
+
+
+def test_mod_mersenne31(bb, golden):
+    for v, r in golden["mod"]:
+        assert bb.mod_mersenne31(int(v)) == int(r)
+
+
+def test_family_errors_and_maps(bb, golden):
+    for e in golden["errors"]:
+        if e["call"] != "family":
+            continue
+        args = [int(a) for a in e["args"]]
+        if args[0] == 0 and args[1] * args[2] * 4 > (1 << 34):
+            pass
+        try:
+            f = bb.Family(*args)
+            st, msg = 0, ""
+            f.close()
+        except bb.BbmhError as ex:
+            st, msg = ex.status, ex.message
+        assert (st, msg) == (e["status"], e["message"]), e
+    f = bb.Family(1, 1 << 16, 3, 42)
+    for e in golden["errors"]:
+        if e["call"] == "map":
+            try:
+                v = f.map(int(e["args"][0]), int(e["args"][1]))
+                st, msg = 0, ""
+                assert v == e["value"]
+            except bb.BbmhError as ex:
+                st, msg = ex.status, ex.message
+            assert (st, msg) == (e["status"], e["message"])
+    for fam in golden["families"]:
+        with bb.Family(fam["scheme"], int(fam["dim"]), fam["k"], int(fam["seed"]),
+                       int(fam["prime"])) as f:
+            for j, t, v in fam["maps"]:
+                assert f.map(j, t) == v
+
+
+def test_b_validation_precedes_device_work(bb, golden):
+    """b outside 1..32 (after the u8 narrowing) is rejected before any CUDA call."""
+    f = bb.Family(1, 1 << 16, 3, 42)
+    for e in golden["errors"]:
+        if e["call"] == "sketch_set" and e["status"] != 0:
+            with pytest.raises(bb.BbmhError) as ex:
+                f.sketch_set([1, 2, 3], int(e["args"][0]))
+            assert (ex.value.status, ex.value.message) == (e["status"], e["message"])
+
+
+def test_compute_fails_loudly_without_gpu(bb):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    f = bb.Family(1, 1 << 16, 3, 42)
+    with pytest.raises(bb.BbmhError) as ex:
+        f.sketch_set([1, 2, 3], 8)
+    assert ex.value.status == bb.E_INTERNAL
+    assert "CUDA" in ex.value.message
+
+
+def test_out_of_scope_symbols_report_not_provided(bb):
+    import ctypes as C
+    L = bb.lib()
+    fn = L.bbmh_train
+    fn.restype = C.c_int32
+    assert fn(None, None, None, None, None) == bb.E_INTERNAL
+    assert "not provided" in bb.last_error()

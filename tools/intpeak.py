@@ -1,0 +1,49 @@
+"""Measures the B200 integer-pipe throughputs that bound the sketch kernels.
+
+Runs paper_1205_2958_b200/libbbmh_intpeak.so (csrc/intpeak.cu) on cuda:0 and
+prints/writes int_peaks.json: per microbenchmark, instructions per SM clock
+(from per-CTA clock64) and Gops/s (from CUDA events).
+    python tools/intpeak.py [out.json]
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+LIB = os.path.join(ROOT, "paper_1205_2958_b200", "libbbmh_intpeak.so")
+OPS = {0: "imad", 1: "imad_wide+lea_hi", 2: "vimnmx3", 3: "iadd3", 4: "lop3",
+       5: "mix_2u(2imad:1vimnmx3)", 6: "lea_hi", 7: "viaddmnmx"}
+SMS = 148
+
+
+def measure(blocks_per_sm=8, threads=256):
+    L = C.CDLL(LIB)
+    L.bbmh_intpeak_run.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float),
+                                   C.POINTER(C.c_double)]
+    L.bbmh_intpeak_ops_per_thread.restype = C.c_double
+    L.bbmh_intpeak_ops_per_thread.argtypes = [C.c_int]
+    res = {}
+    blocks = SMS * blocks_per_sm
+    for op, name in OPS.items():
+        ms, cyc = C.c_float(), C.c_double()
+        st = L.bbmh_intpeak_run(op, blocks, threads, C.byref(ms), C.byref(cyc))
+        if st != 0:
+            res[name] = {"error": st}
+            continue
+        per_thread = L.bbmh_intpeak_ops_per_thread(op)
+        total = per_thread * threads * blocks
+        per_sm_clk = per_thread * threads * blocks_per_sm / cyc.value
+        res[name] = {"inst_per_clk_per_sm": round(per_sm_clk, 2),
+                     "gops": round(total / (ms.value * 1e-3) / 1e9, 1),
+                     "implied_mhz": round(cyc.value / (ms.value * 1e-3) / 1e6, 0),
+                     "ms": round(ms.value, 3)}
+    return {"sms": SMS, "blocks_per_sm": blocks_per_sm, "threads": threads, "ops": res}
+
+
+if __name__ == "__main__":
+    r = measure()
+    print(json.dumps(r, indent=1))
+    if len(sys.argv) > 1:
+        with open(sys.argv[1], "w") as f:
+            json.dump(r, f, indent=1)
