@@ -46,8 +46,6 @@ K = 500
 B = 8
 SEED = 42
 SCHEMES = {"2u": (1, D_2U), "4u-bit": (3, D_WEBSPAM), "4u-mod": (2, D_WEBSPAM)}
-# SASS instructions per hash evaluation in the inner loop: fma-pipe, alu-pipe
-INST_PER_EVAL = {"2u": (1.0, 0.5), "4u-bit": (3.0, 8.5), "4u-mod": (None, None)}
 
 
 def log(*a):
@@ -151,24 +149,46 @@ def int_peaks():
     return intpeak.measure()
 
 
-def roofline_int(scheme, evals_per_s, sm_mhz, peaks):
-    """Issue-pipe roofline of the sketch kernel: each evaluation needs `fma`
-    FMA-pipe and `alu` ALU-pipe instructions (SASS of the inner loop); the
-    bound is the slower pipe at the measured per-SM rate and the SM clock
-    seen under load."""
-    fma, alu = INST_PER_EVAL[scheme]
+def pipe_costs(scheme, dim, peaks):
+    """Per-evaluation cost of the inner loop on the two integer pipes, in
+    issue slots of a full-rate instruction. From the SASS:
+      2U     : 1 IMAD (fma-heavy) + 1/2 VIMNMX3 (alu)
+      4U-bit : 3 x [IMAD.WIDE (fma) + LEA.HI (alu)] + 4 VIADDMNMX (alu, lazy and
+               canonical Mersenne reductions) + 1/2 VIMNMX3, then `mod D`:
+               LOP3 (alu) for power-of-two D, else IMAD.HI + IMAD (fma) + SHF (alu).
+    Multi-cycle fma instructions (IMAD.WIDE, IMAD.HI) are charged at their
+    measured rate relative to IMAD."""
+    ops = peaks["ops"]
+    imad = ops["imad"]["inst_per_clk_per_sm"]
+    wide = imad / ops["imad_wide+lop3"]["inst_per_clk_per_sm"] * 2  # pair = wide + lop3
+    hi = imad / ops["imad_hi"]["inst_per_clk_per_sm"]
+    if scheme == "2u":
+        return 1.0, 0.5
+    if scheme == "4u-bit":
+        pow2 = dim & (dim - 1) == 0
+        fma = 3 * wide + (0 if pow2 else hi + 1)
+        alu = 3 + 4 + 1 + 0.5
+        return fma, alu
+    return None, None
+
+
+def roofline_int(scheme, dim, evals_per_s, sm_mhz, peaks):
+    """Integer-pipe roofline of the sketch kernel: the slower of the fma-heavy
+    and alu pipes at their measured per-SM rates and the SM clock under load."""
+    fma, alu = pipe_costs(scheme, dim, peaks)
     if fma is None or not sm_mhz:
         return None
     ops = peaks["ops"]
     fma_rate = ops["imad"]["inst_per_clk_per_sm"]
-    alu_rate = max(ops["vimnmx3"]["inst_per_clk_per_sm"], ops["lop3"]["inst_per_clk_per_sm"])
+    alu_rate = ops["vimnmx3"]["inst_per_clk_per_sm"]
     evals_per_clk = min(fma_rate / fma, alu_rate / alu)
     peak = 148 * evals_per_clk * sm_mhz * 1e6
     return {"bound": "int", "unit": "Gevals/s", "achieved": evals_per_s / 1e9,
             "peak": peak / 1e9, "frac": evals_per_s / peak,
-            "inst_per_eval": {"fma_pipe": fma, "alu_pipe": alu},
-            "pipe_rates_per_sm_clk": {"fma": fma_rate, "alu": alu_rate},
-            "sm_mhz": sm_mhz}
+            "slots_per_eval": {"fma_heavy": round(fma, 3), "alu": alu},
+            "pipe_rates_per_sm_clk": {"fma_heavy": fma_rate, "alu": alu_rate},
+            "binding_pipe": "fma_heavy" if fma_rate / fma <= alu_rate / alu else "alu",
+            "sm_mhz": sm_mhz, "peaks": "measured by tools/intpeak.py in this run"}
 
 
 # ---- the two arms -----------------------------------------------------------------
@@ -184,7 +204,12 @@ def run_reference(args):
         return
     scheme_id, dim = SCHEMES[args.scheme]
     threads = os.cpu_count() or 1
-    n_sample = args.ref_docs or max(64, 12 * threads)
+    nc = 4 * threads
+    rp, idx = make_corpus_host(nc, NNZ, D_WEBSPAM, SEED)
+    tc, _ = O.refbench_sketch_csr(O.REF_SO, scheme_id, dim, K, SEED, rp, idx, B, threads)
+    # each step is a bounded sample sized for ~args.cpu_seconds / steps of CPU work
+    per_step = args.cpu_seconds * 2 / max(1, args.steps)
+    n_sample = args.ref_docs or int(min(N_DOCS, max(nc, nc * per_step / max(tc, 1e-3))))
     rp, idx = make_corpus_host(n_sample, NNZ, D_WEBSPAM, SEED)
     evals = n_sample * NNZ * K
     # warm-up on a small slice, then K timed steps over the sample
@@ -286,7 +311,7 @@ def run_ours(args):
                          "ms_per_step": ms, "kernel_ms_min": min(per), "kernel_ms_max": max(per),
                          "sm_mhz": clk["sm_mhz"]}
         if rank == 0:
-            rl = roofline_int(name, evals / (ms * 1e-3), clk["sm_mhz"], peaks)
+            rl = roofline_int(name, dim, evals / (ms * 1e-3), clk["sm_mhz"], peaks)
             results[name]["roofline"] = rl
             alg_bytes = n * nnz * 4 + (n + 1) * 8 + n * cb + n
             results[name]["hbm_gbs_algorithmic"] = alg_bytes / (ms * 1e-3) / 1e9
@@ -326,10 +351,13 @@ def run_ours(args):
         from oracle import oracle as O
         if O.ref_available():
             threads = os.cpu_count() or 1
-            ns = args.ref_docs or max(64, 12 * threads)
+            # calibrate on a few docs, then size the sample for ~args.cpu_seconds of work
+            nc = 4 * threads
+            tc, _ = O.refbench_sketch_csr(O.REF_SO, 1, D_2U, K, SEED, h_rp[: nc + 1].copy(),
+                                          pin.array[: nc * nnz].copy(), B, threads)
+            ns = args.ref_docs or int(min(n, max(nc, nc * args.cpu_seconds / max(tc, 1e-3))))
             srp = h_rp[: ns + 1].copy()
             sidx = pin.array[: ns * nnz].copy()
-            O.refbench_sketch_csr(O.REF_SO, 1, D_2U, K, SEED, srp[:3], sidx[: 2 * nnz], B, threads)
             secs, ref_codes = O.refbench_sketch_csr(O.REF_SO, 1, D_2U, K, SEED, srp, sidx, B, threads)
             parity = bool(np.array_equal(ref_codes.reshape(-1), codes_out.array[: ns * cb]))
             cpu = {"value": ns * nnz * K / secs, "unit": "hash-evals/s", "cores": threads,
@@ -382,6 +410,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-docs", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -13,7 +13,7 @@
 namespace {
 
 constexpr int kIlp = 8;
-constexpr int kIters = 4096;
+constexpr int kIters = 32768;
 
 enum Op : int {
     OP_IMAD = 0,       // IMAD R, R, R, R          (fma pipe)
@@ -24,11 +24,14 @@ enum Op : int {
     OP_MIX_2U = 5,     // 2 IMAD : 1 VIMNMX3 -- the 2U inner loop mix
     OP_LEAHI = 6,      // LEA.HI (hi + lo>>1)      (alu pipe)
     OP_VIADDMNMX = 7,  // min(x + c, x)            (alu pipe)
+    OP_WIDE_XOR = 8,   // IMAD.WIDE.U32 + LOP3     (64-bit product rate)
+    OP_IMAD_HI = 9,    // IMAD.HI.U32              (high-word product rate)
 };
 
 template <int OP>
 __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* sink,
-                                                     unsigned long long* cycles) {
+                                                     unsigned long long* cycles,
+                                                     unsigned long long* clk) {
     uint32_t a[kIlp], c1 = seed * 3 + 1, c2 = seed ^ 0x9e3779b9u;
     uint64_t w[kIlp];
 #pragma unroll
@@ -37,6 +40,8 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
         w[i] = a[i];
     }
     __syncthreads();
+    unsigned long long g0 = 0, g1 = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
     const unsigned long long t0 = clock64();
     for (int it = 0; it < kIters; ++it) {
 #pragma unroll
@@ -64,13 +69,26 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
             } else if constexpr (OP == OP_LEAHI) {
                 a[i] = c1 + (a[i] >> 1);
                 asm volatile("" : "+r"(a[i]));
-            } else {
+            } else if constexpr (OP == OP_VIADDMNMX) {
                 a[i] = min(a[i] + 0x80000001u, a[i]);
                 asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_WIDE_XOR) {
+                const uint64_t v = (uint64_t)a[i] * c1 + c2;
+                a[i] = (uint32_t)(v >> 32) ^ (uint32_t)v;
+                asm volatile("" : "+r"(a[i]));
+            } else {
+                asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(c1), "r"(c2));
             }
         }
     }
     const unsigned long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+        clk[0] = t0;
+        clk[1] = t1;
+        clk[2] = g0;
+        clk[3] = g1;
+    }
     uint32_t acc = 0;
 #pragma unroll
     for (int i = 0; i < kIlp; ++i) acc ^= a[i] ^ (uint32_t)w[i] ^ (uint32_t)(w[i] >> 32);
@@ -79,13 +97,14 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
 }
 
 template <int OP>
-float run(int blocks, int threads, uint32_t* sink, unsigned long long* cyc, cudaStream_t st) {
+float run(int blocks, int threads, uint32_t* sink, unsigned long long* cyc, unsigned long long* clk,
+          cudaStream_t st) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    intpeak_kernel<OP><<<blocks, threads, 0, st>>>(1, sink, cyc);  // warm-up
+    intpeak_kernel<OP><<<blocks, threads, 0, st>>>(1, sink, cyc, clk);  // warm-up
     cudaEventRecord(e0, st);
-    intpeak_kernel<OP><<<blocks, threads, 0, st>>>(2, sink, cyc);
+    intpeak_kernel<OP><<<blocks, threads, 0, st>>>(2, sink, cyc, clk);
     cudaEventRecord(e1, st);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -106,29 +125,35 @@ __attribute__((visibility("default"))) double bbmh_intpeak_ops_per_thread(int op
     switch (op) {
         case OP_MIX_2U: return base * 3;  // 2 IMAD + 1 VIMNMX3
         case OP_IMAD_WIDE: return base * 2;  // IMAD.WIDE + LEA.HI
+        case OP_WIDE_XOR: return base * 2;   // IMAD.WIDE + LOP3
         default: return base;
     }
 }
 
 // Runs one microbenchmark; returns elapsed ms and the mean per-CTA cycles.
 __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, int threads,
-                                                           float* ms_out, double* cycles_out) {
+                                                           float* ms_out, double* cycles_out,
+                                                           double* sm_mhz_out) {
     uint32_t* sink = nullptr;
     unsigned long long* cyc = nullptr;
+    unsigned long long* clk = nullptr;
     if (cudaMalloc(&sink, 4) != cudaSuccess) return -1;
+    if (cudaMalloc(&clk, 4 * sizeof(unsigned long long)) != cudaSuccess) return -1;
     if (cudaMalloc(&cyc, sizeof(unsigned long long) * blocks) != cudaSuccess) return -1;
     cudaStream_t st;
     cudaStreamCreate(&st);
     float ms = -1;
     switch (op) {
-        case OP_IMAD: ms = run<OP_IMAD>(blocks, threads, sink, cyc, st); break;
-        case OP_IMAD_WIDE: ms = run<OP_IMAD_WIDE>(blocks, threads, sink, cyc, st); break;
-        case OP_VIMNMX3: ms = run<OP_VIMNMX3>(blocks, threads, sink, cyc, st); break;
-        case OP_IADD3: ms = run<OP_IADD3>(blocks, threads, sink, cyc, st); break;
-        case OP_LOP3: ms = run<OP_LOP3>(blocks, threads, sink, cyc, st); break;
-        case OP_MIX_2U: ms = run<OP_MIX_2U>(blocks, threads, sink, cyc, st); break;
-        case OP_LEAHI: ms = run<OP_LEAHI>(blocks, threads, sink, cyc, st); break;
-        case OP_VIADDMNMX: ms = run<OP_VIADDMNMX>(blocks, threads, sink, cyc, st); break;
+        case OP_IMAD: ms = run<OP_IMAD>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_IMAD_WIDE: ms = run<OP_IMAD_WIDE>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_VIMNMX3: ms = run<OP_VIMNMX3>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_IADD3: ms = run<OP_IADD3>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_LOP3: ms = run<OP_LOP3>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_2U: ms = run<OP_MIX_2U>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_LEAHI: ms = run<OP_LEAHI>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_VIADDMNMX: ms = run<OP_VIADDMNMX>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_WIDE_XOR: ms = run<OP_WIDE_XOR>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_IMAD_HI: ms = run<OP_IMAD_HI>(blocks, threads, sink, cyc, clk, st); break;
         default: return -2;
     }
     unsigned long long* h = new unsigned long long[blocks];
@@ -138,6 +163,10 @@ __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, 
     delete[] h;
     *ms_out = ms;
     *cycles_out = s / blocks;
+    unsigned long long hc[4];
+    cudaMemcpy(hc, clk, sizeof hc, cudaMemcpyDeviceToHost);
+    *sm_mhz_out = hc[3] > hc[2] ? double(hc[1] - hc[0]) / double(hc[3] - hc[2]) * 1e3 : 0;
+    cudaFree(clk);
     cudaFree(sink);
     cudaFree(cyc);
     cudaStreamDestroy(st);

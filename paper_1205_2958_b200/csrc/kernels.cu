@@ -153,33 +153,128 @@ __device__ __forceinline__ uint32_t hash1(const KernelFamily& F, const Coef<SCHE
     }
 }
 
+// ---- TMA bulk copy + mbarrier helpers (sm_90+ PTX; SASS: UBLKCP / SYNCS) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// One unit of pipelined work: up to kTile ids of one document.
+struct Item {
+    uint64_t doc;
+    uint32_t cnt;    // ids in this tile (0 for an empty document)
+    uint32_t head;   // garbage ids before the first one (16-byte alignment of the copy)
+    uint32_t first;  // first tile of the document
+    uint32_t last;   // last tile (run the epilogue)
+    uint32_t empty;  // document has no ids
+    uint32_t valid;  // 0 = no more work for this CTA
+};
+
+constexpr uint32_t kBuf = kTile + 8;  // room for the 16-byte head/tail slack
+
+// Persistent sketch kernel. Each CTA walks documents blockIdx.x,
+// blockIdx.x + gridDim.x, ... for hash-function tile blockIdx.y. Thread 0 is
+// the producer: it issues one TMA bulk copy per item into one of two shared
+// buffers (completion signalled on an mbarrier) one item ahead, so the next
+// document's ids land while the current one is hashed.
 template <int SCHEME, bool POW2, int J>
 __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint64_t* __restrict__ row_ptr,
                                                      uint64_t index_base,
                                                      const uint32_t* __restrict__ indices,
-                                                     uint32_t b, uint32_t jtile,
+                                                     uint64_t n_docs, uint32_t b, uint32_t jtile,
                                                      uint8_t* __restrict__ codes,
                                                      uint64_t* __restrict__ minima,
                                                      uint8_t* __restrict__ flags, int* err) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* s_idx = smem;           // kTile staged ids
-    uint32_t* s_code = smem + kTile;  // jtile codes
-    const uint4* s_idx4 = reinterpret_cast<const uint4*>(s_idx);
+    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t* s_code = smem + 2 * kBuf;  // jtile codes
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ Item desc[2];
 
-    const uint64_t doc = blockIdx.x;
     const uint32_t tid = threadIdx.x;
     const uint32_t tpb = blockDim.x;
     const uint32_t k = F.k;
     const uint32_t j0 = blockIdx.y * jtile;
+    const uint32_t jcnt = min(jtile, k - j0);
 
-    uint64_t beg = row_ptr[doc], end = row_ptr[doc + 1];
-    if (end < beg) {
-        if (tid == 0) atomicOr(err, 2);
-        end = beg;
+    // ---- producer state (thread 0 only) ----
+    uint64_t p_doc = blockIdx.x, p_off = 0, p_beg = 0, p_end = 0;
+    auto load_bounds = [&]() {
+        if (p_doc < n_docs) {
+            p_beg = row_ptr[p_doc];
+            p_end = row_ptr[p_doc + 1];
+            if (p_end < p_beg) {
+                atomicOr(err, 2);
+                p_end = p_beg;
+            }
+        }
+    };
+    auto issue = [&](int bi) {
+        Item it{};
+        if (p_doc >= n_docs) {
+            it.valid = 0;
+            desc[bi] = it;
+            return;
+        }
+        const uint64_t nnz = p_end - p_beg;
+        const uint64_t rem = nnz - p_off;
+        it.valid = 1;
+        it.doc = p_doc;
+        it.first = p_off == 0;
+        it.empty = nnz == 0;
+        it.cnt = (uint32_t)(rem < kTile ? rem : kTile);
+        it.last = p_off + it.cnt >= nnz;
+        if (it.cnt) {
+            const uint32_t* src = indices + (p_beg - index_base) + p_off;
+            const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+            it.head = (uint32_t)(((uintptr_t)src - a0) >> 2);
+            const uint32_t bytes = ((it.head + it.cnt) * 4 + 15) & ~15u;
+            // order earlier generic-proxy writes to this buffer before the async-proxy copy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&mbar[bi], bytes);
+            tma_bulk_g2s(smem + bi * kBuf, reinterpret_cast<const void*>(a0), bytes, &mbar[bi]);
+        }
+        desc[bi] = it;
+        if (it.last) {
+            p_doc += gridDim.x;
+            p_off = 0;
+            load_bounds();
+        } else {
+            p_off += it.cnt;
+        }
+    };
+
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        load_bounds();
+        issue(0);
     }
-    beg -= index_base;
-    end -= index_base;
-    const uint64_t nnz = end - beg;
+    __syncthreads();
 
     Coef<SCHEME> c[J];
     uint32_t m[J];
@@ -189,68 +284,93 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         c[r].load(F, j);
         m[r] = 0xffffffffu;
     }
+    const uint32_t mask = b >= 32 ? 0xffffffffu : ((1u << b) - 1);
+    const uint64_t cb = ((uint64_t)k * b + 7) >> 3;
+    uint32_t phase = 0;  // bit i = parity of the next completion of mbar[i]
 
-    for (uint64_t off = 0; off < nnz; off += kTile) {
-        const uint32_t cnt = (uint32_t)(nnz - off < kTile ? nnz - off : kTile);
-        const uint32_t cnt4 = (cnt + 3) & ~3u;
-        const uint32_t* src = indices + beg + off;
-        for (uint32_t i = tid; i < cnt4; i += tpb) {
-            const uint32_t t = __ldg(src + (i < cnt ? i : 0));  // pad with a duplicate id
-            s_idx[i] = stage_transform<SCHEME>(F, t, err);
-        }
-        __syncthreads();
-        const uint32_t n4 = cnt4 >> 2;
-#pragma unroll 2
-        for (uint32_t q = 0; q < n4; ++q) {
-            const uint4 t4 = s_idx4[q];
+    for (uint32_t itn = 0;; ++itn) {
+        const int bi = itn & 1;
+        const Item d = desc[bi];
+        if (!d.valid) break;
+        if (tid == 0) issue(bi ^ 1);  // prefetch the next item into the other buffer
+        if (d.first) {
 #pragma unroll
-            for (int r = 0; r < J; ++r) {
-                const uint32_t h0 = hash1<SCHEME, POW2>(F, c[r], t4.x);
-                const uint32_t h1 = hash1<SCHEME, POW2>(F, c[r], t4.y);
-                const uint32_t h2 = hash1<SCHEME, POW2>(F, c[r], t4.z);
-                const uint32_t h3 = hash1<SCHEME, POW2>(F, c[r], t4.w);
-                m[r] = min3u(m[r], h0, h1);
-                m[r] = min3u(m[r], h2, h3);
+            for (int r = 0; r < J; ++r) m[r] = 0xffffffffu;
+        }
+        if (d.cnt) {
+            uint32_t* buf = smem + bi * kBuf;
+            mbar_wait(&mbar[bi], (phase >> bi) & 1);
+            phase ^= 1u << bi;
+            const uint32_t lo = d.head, hi = d.head + d.cnt;
+            const uint32_t n4 = (hi + 3) >> 2;
+            constexpr bool kTransform = SCHEME != S_2U;
+            if (kTransform || lo != 0 || (hi & 3) != 0) {
+                // pad the alignment slack with a duplicate id (min unaffected) and
+                // pre-transform ids in place (t mod p, doubled for 4U-bit)
+                const uint32_t first = buf[lo];
+                if (kTransform) __syncthreads();  // everyone read `first` before rewriting
+                for (uint32_t i = tid; i < 4 * n4; i += tpb) {
+                    const uint32_t t = (i < lo || i >= hi) ? first : buf[i];
+                    if (kTransform || i < lo || i >= hi) buf[i] = stage_transform<SCHEME>(F, t, err);
+                }
+                __syncthreads();
+            }
+            const uint4* b4 = reinterpret_cast<const uint4*>(buf);
+#pragma unroll 2
+            for (uint32_t q = 0; q < n4; ++q) {
+                const uint4 t4 = b4[q];
+#pragma unroll
+                for (int r = 0; r < J; ++r) {
+                    const uint32_t h0 = hash1<SCHEME, POW2>(F, c[r], t4.x);
+                    const uint32_t h1 = hash1<SCHEME, POW2>(F, c[r], t4.y);
+                    const uint32_t h2 = hash1<SCHEME, POW2>(F, c[r], t4.z);
+                    const uint32_t h3 = hash1<SCHEME, POW2>(F, c[r], t4.w);
+                    m[r] = min3u(m[r], h0, h1);
+                    m[r] = min3u(m[r], h2, h3);
+                }
             }
         }
-        __syncthreads();
-    }
-
-    // ---- epilogue: minima -> codes -> packed bitstream (sketch.cpp:80-98) --
-    const bool empty = nnz == 0;
-    const uint32_t mask = b >= 32 ? 0xffffffffu : ((1u << b) - 1);
-    const uint32_t jcnt = min(jtile, k - j0);
+        if (d.last) {
+            // ---- epilogue: minima -> codes -> packed bitstream (sketch.cpp:80-98) ----
+            const uint64_t doc = d.doc;
+            const bool empty = d.empty;
 #pragma unroll
-    for (int r = 0; r < J; ++r) {
-        const uint32_t jl = tid + r * tpb;
-        if (jl < jcnt) {
-            uint32_t mn = m[r];
-            if constexpr (SCHEME == S_2U) mn >>= F.shift2u;
-            s_code[jl] = empty ? mask : (mn & mask);
-            if (minima) minima[doc * k + j0 + jl] = empty ? ~0ull : (uint64_t)mn;
+            for (int r = 0; r < J; ++r) {
+                const uint32_t jl = tid + r * tpb;
+                if (jl < jcnt) {
+                    uint32_t mn = m[r];
+                    if constexpr (SCHEME == S_2U) mn >>= F.shift2u;
+                    s_code[jl] = empty ? mask : (mn & mask);
+                    if (minima) minima[doc * k + j0 + jl] = empty ? ~0ull : (uint64_t)mn;
+                }
+            }
+            if (flags && blockIdx.y == 0 && tid == 0) flags[doc] = empty ? 1 : 0;
+            __syncthreads();
+            const uint64_t byte0 = ((uint64_t)j0 * b) >> 3;  // j0*b is a multiple of 8
+            const uint64_t byte1e = ((uint64_t)(j0 + jcnt) * b + 7) >> 3;
+            const uint64_t byte1 = byte1e < cb ? byte1e : cb;
+            uint8_t* out = codes + doc * cb;
+            for (uint64_t B = byte0 + tid; B < byte1; B += tpb) {
+                const uint64_t bit0 = B << 3;
+                const uint32_t ja = (uint32_t)(bit0 / b);
+                const uint64_t jb0 = (bit0 + 7) / b, jlast = (uint64_t)j0 + jcnt - 1;
+                const uint32_t jb = (uint32_t)(jb0 < jlast ? jb0 : jlast);
+                uint32_t v = 0;
+                for (uint32_t j = ja; j <= jb; ++j) {
+                    const uint64_t code = s_code[j - j0];
+                    const int64_t pos = (int64_t)j * b - (int64_t)bit0;
+                    v |= (uint32_t)(pos >= 0 ? (code << pos) : (code >> -pos));
+                }
+                out[B] = (uint8_t)v;
+            }
         }
+        __syncthreads();  // buffer bi and s_code free; desc[bi ^ 1] visible
     }
-    if (flags && blockIdx.y == 0 && tid == 0) flags[doc] = empty ? 1 : 0;
-    __syncthreads();
+}
 
-    const uint64_t cb = ((uint64_t)k * b + 7) >> 3;
-    const uint64_t byte0 = ((uint64_t)j0 * b) >> 3;  // j0*b is a multiple of 8
-    const uint64_t byte1e = ((uint64_t)(j0 + jcnt) * b + 7) >> 3;
-    const uint64_t byte1 = byte1e < cb ? byte1e : cb;
-    uint8_t* out = codes + doc * cb;
-    for (uint64_t B = byte0 + tid; B < byte1; B += tpb) {
-        const uint64_t bit0 = B << 3;
-        const uint32_t ja = (uint32_t)(bit0 / b);
-        const uint64_t jb0 = (bit0 + 7) / b, jlast = (uint64_t)j0 + jcnt - 1;
-        const uint32_t jb = (uint32_t)(jb0 < jlast ? jb0 : jlast);
-        uint32_t v = 0;
-        for (uint32_t j = ja; j <= jb; ++j) {
-            const uint64_t code = s_code[j - j0];
-            const int64_t pos = (int64_t)j * b - (int64_t)bit0;
-            v |= (uint32_t)(pos >= 0 ? (code << pos) : (code >> -pos));
-        }
-        out[B] = (uint8_t)v;
-    }
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
 }
 
 template <int SCHEME, bool POW2, int J>
@@ -258,17 +378,23 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
                 uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
                 uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
     auto kern = sketch_kernel<SCHEME, POW2, J>;
-    const size_t smem = (kTile + sh.jtile) * sizeof(uint32_t);
-    constexpr uint64_t kMaxGrid = 1u << 30;
-    const size_t cb = ((size_t)F.k * b + 7) / 8;
-    for (uint64_t d0 = 0; d0 < n; d0 += kMaxGrid) {
-        const uint64_t nd = n - d0 < kMaxGrid ? n - d0 : kMaxGrid;
-        dim3 grid((unsigned)nd, sh.jtiles);
-        kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr + d0, base, idx, b, sh.jtile, codes + d0 * cb,
-                                         minima ? minima + d0 * F.k : nullptr,
-                                         flags ? flags + d0 : nullptr, err);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-    }
+    const size_t smem = (2 * kBuf + sh.jtile) * sizeof(uint32_t);
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.tpb, smem);
+    occ = occ < 1 ? 1 : occ;
+    const int ctas_env = env_int("BBMH_TUNE_CTAS_PER_SM", 0);
+    if (ctas_env > 0 && ctas_env < occ) occ = ctas_env;
+    // persistent: one wave of CTAs per j-tile, each looping over documents
+    uint64_t gx = (uint64_t)sms * occ / sh.jtiles;
+    if (gx < 1) gx = 1;
+    if (gx > n) gx = n;
+    dim3 grid((unsigned)gx, sh.jtiles);
+    kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr, base, idx, n, b, sh.jtile, codes, minima, flags,
+                                     err);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 template <int SCHEME, bool POW2>
@@ -283,10 +409,6 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     }
 }
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? std::atoi(v) : dflt;
-}
 
 }  // namespace
 

@@ -13,30 +13,32 @@ import sys
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 LIB = os.path.join(ROOT, "paper_1205_2958_b200", "libbbmh_intpeak.so")
 OPS = {0: "imad", 1: "imad_wide+lea_hi", 2: "vimnmx3", 3: "iadd3", 4: "lop3",
-       5: "mix_2u(2imad:1vimnmx3)", 6: "lea_hi", 7: "viaddmnmx"}
+       5: "mix_2u(2imad:1vimnmx3)", 6: "lea_hi", 7: "viaddmnmx", 8: "imad_wide+lop3",
+       9: "imad_hi"}
 SMS = 148
 
 
 def measure(blocks_per_sm=8, threads=256):
     L = C.CDLL(LIB)
     L.bbmh_intpeak_run.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float),
-                                   C.POINTER(C.c_double)]
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.bbmh_intpeak_ops_per_thread.restype = C.c_double
     L.bbmh_intpeak_ops_per_thread.argtypes = [C.c_int]
     res = {}
     blocks = SMS * blocks_per_sm
     for op, name in OPS.items():
-        ms, cyc = C.c_float(), C.c_double()
-        st = L.bbmh_intpeak_run(op, blocks, threads, C.byref(ms), C.byref(cyc))
+        ms, cyc, mhz = C.c_float(), C.c_double(), C.c_double()
+        st = L.bbmh_intpeak_run(op, blocks, threads, C.byref(ms), C.byref(cyc), C.byref(mhz))
         if st != 0:
             res[name] = {"error": st}
             continue
         per_thread = L.bbmh_intpeak_ops_per_thread(op)
         total = per_thread * threads * blocks
-        per_sm_clk = per_thread * threads * blocks_per_sm / cyc.value
-        res[name] = {"inst_per_clk_per_sm": round(per_sm_clk, 2),
-                     "gops": round(total / (ms.value * 1e-3) / 1e9, 1),
-                     "implied_mhz": round(cyc.value / (ms.value * 1e-3) / 1e6, 0),
+        gops = total / (ms.value * 1e-3) / 1e9
+        # instructions per SM clock: whole-kernel rate / (SMs x measured SM clock)
+        per_sm_clk = gops * 1e9 / (SMS * mhz.value * 1e6) if mhz.value else None
+        res[name] = {"inst_per_clk_per_sm": round(per_sm_clk, 2) if per_sm_clk else None,
+                     "gops": round(gops, 1), "sm_mhz": round(mhz.value, 1),
                      "ms": round(ms.value, 3)}
     return {"sms": SMS, "blocks_per_sm": blocks_per_sm, "threads": threads, "ops": res}
 
