@@ -33,7 +33,7 @@ namespace bbmh {
 
 namespace {
 
-constexpr uint32_t kTile = 4096;  // feature ids staged per pass (16 KB)
+constexpr uint32_t kDefaultTile = 4096;  // feature ids staged per pipeline item (16 KB)
 constexpr uint32_t kP31 = 0x7fffffffu;
 
 std::atomic<uint64_t> g_launches{0};
@@ -183,7 +183,7 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
         : "memory");
 }
 
-// One unit of pipelined work: up to kTile ids of one document.
+// One unit of pipelined work: up to `tile` ids of one document.
 struct Item {
     uint64_t doc;
     uint32_t cnt;    // ids in this tile (0 for an empty document)
@@ -194,7 +194,7 @@ struct Item {
     uint32_t valid;  // 0 = no more work for this CTA
 };
 
-constexpr uint32_t kBuf = kTile + 8;  // room for the 16-byte head/tail slack
+// each buffer holds tile + 8 ids: room for the 16-byte head/tail slack
 
 // Persistent sketch kernel. Each CTA walks documents blockIdx.x,
 // blockIdx.x + gridDim.x, ... for hash-function tile blockIdx.y. Thread 0 is
@@ -206,10 +206,12 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
                                                      uint64_t index_base,
                                                      const uint32_t* __restrict__ indices,
                                                      uint64_t n_docs, uint32_t b, uint32_t jtile,
+                                                     uint32_t tile,
                                                      uint8_t* __restrict__ codes,
                                                      uint64_t* __restrict__ minima,
                                                      uint8_t* __restrict__ flags, int* err) {
     extern __shared__ __align__(128) uint32_t smem[];
+    const uint32_t kBuf = tile + 8;
     uint32_t* s_code = smem + 2 * kBuf;  // jtile codes
     __shared__ __align__(8) uint64_t mbar[2];
     __shared__ Item desc[2];
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         it.doc = p_doc;
         it.first = p_off == 0;
         it.empty = nnz == 0;
-        it.cnt = (uint32_t)(rem < kTile ? rem : kTile);
+        it.cnt = (uint32_t)(rem < tile ? rem : tile);
         it.last = p_off + it.cnt >= nnz;
         if (it.cnt) {
             const uint32_t* src = indices + (p_beg - index_base) + p_off;
@@ -378,7 +380,9 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
                 uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
                 uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
     auto kern = sketch_kernel<SCHEME, POW2, J>;
-    const size_t smem = (2 * kBuf + sh.jtile) * sizeof(uint32_t);
+    int tile = env_int("BBMH_TUNE_TILE", SCHEME == S_2U ? 1024 : (int)kDefaultTile);
+    tile = tile < 64 ? 64 : tile > 16384 ? 16384 : tile & ~3;
+    const size_t smem = (2 * (tile + 8) + sh.jtile) * sizeof(uint32_t);
     int dev = 0, sms = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -392,8 +396,8 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     if (gx < 1) gx = 1;
     if (gx > n) gx = n;
     dim3 grid((unsigned)gx, sh.jtiles);
-    kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr, base, idx, n, b, sh.jtile, codes, minima, flags,
-                                     err);
+    kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr, base, idx, n, b, sh.jtile, (uint32_t)tile, codes,
+                                     minima, flags, err);
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -413,23 +417,24 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
 }  // namespace
 
 LaunchShape choose_shape(uint32_t k, int scheme) {
-    // Minimise idle (j >= k) lanes; among equal slot counts prefer J = 4
-    // (one LDS.128 feeds 16 evaluations) and fewer CTAs per document.
-    (void)scheme;
+    // Cost = lane-slots (tiles * tpb * J, idle j >= k lanes included) scaled by
+    // the measured relative inefficiency of small J (one LDS.128 feeds 4*J
+    // evaluations; tools/tune.py, profiles/r02): 2U is issue-bound so J = 1
+    // costs ~30% and J = 8 is best; 4U is arithmetic-bound and flat in J.
+    // Ties prefer fewer CTAs per document.
     LaunchShape best;
-    uint64_t best_slots = ~0ull;
-    int best_pen = 1 << 30;
-    const int Js[4] = {4, 8, 2, 1};
+    double best_cost = 1e300;
+    const int Js[4] = {8, 4, 2, 1};
     for (int J : Js) {
+        const double eff = scheme == S_2U ? (J == 8 ? 1.0 : J == 4 ? 1.06 : J == 2 ? 1.1 : 1.35)
+                                          : (J == 2 ? 1.0 : J == 4 ? 1.01 : J == 8 ? 1.02 : 1.02);
         for (int tpb = 32; tpb <= 256; tpb += 32) {
             const uint64_t jtile = (uint64_t)tpb * J;
             const uint64_t tiles = (k + jtile - 1) / jtile;
             if (tiles > 65535) continue;
-            const uint64_t slots = tiles * jtile;
-            const int pen = (int)tiles * 4 + (J == 4 ? 0 : J == 8 ? 1 : J == 2 ? 2 : 3);
-            if (slots < best_slots || (slots == best_slots && pen < best_pen)) {
-                best_slots = slots;
-                best_pen = pen;
+            const double cost = (double)(tiles * jtile) * eff * (1.0 + 0.01 * (double)tiles);
+            if (cost < best_cost) {
+                best_cost = cost;
                 best.J = J;
                 best.tpb = tpb;
                 best.jtile = (uint32_t)jtile;
