@@ -224,6 +224,29 @@ def main():
             g["expand_errors"].append({"path": os.path.basename(path), "fmt": fmt, "status": s,
                                        "message": R.last_error().replace(td + "/", "")})
 
+    # Config 1 at full size: the reference's own generator
+    # bbmh_synth_classification(n=20000, D=2^24, density=3700/D, noise 0.3, seed 1,
+    # BBCV) and the reference's sketch files for 2U and 4U-bit, k=200, b=8, seed 42.
+    import ctypes as C
+    L = R.lib
+    L.bbmh_synth_classification.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_double,
+                                            C.c_double, C.c_double, C.c_uint64, C.c_int32]
+    with tempfile.TemporaryDirectory() as td:
+        corpus = os.path.join(td, "c1.bbcv")
+        assert L.bbmh_synth_classification(corpus.encode(), 20000, 1 << 24, 3700 / (1 << 24),
+                                           0.3, 0.0, 1, 1) == 0
+        c1 = {"synth": [20000, 1 << 24, 3700 / (1 << 24), 0.3, 0.0, 1, 1],
+              "corpus_sha256": hashlib.sha256(open(corpus, "rb").read()).hexdigest(),
+              "k": 200, "b": 8, "seed": 42, "dim": 1 << 24, "sketch_sha256": {}}
+        for scheme in (1, 3):
+            st, h = R.family(scheme, 1 << 24, 200, 42)
+            out = os.path.join(td, f"c1_{scheme}.bbmh")
+            s, _ = R.sketch_file(h, corpus, out, 8, 500, os.cpu_count() or 1, False)
+            assert s == 0
+            c1["sketch_sha256"][str(scheme)] = hashlib.sha256(open(out, "rb").read()).hexdigest()
+            R.destroy(h)
+        g["c1"] = c1
+
     with open(OUT, "w") as f:
         json.dump(g, f, separators=(",", ":"))
     print(OUT, os.path.getsize(OUT), "bytes")

@@ -273,3 +273,25 @@ def test_file_bytes_independent_of_batching(bb, tmp_path):
         outs.append(open(o, "rb").read())
     bb.set_chunk_docs(0)
     assert all(x == outs[0] for x in outs)
+
+
+def test_config1_full_size_digests(bb, ref, golden, tmp_path):
+    """BASELINE config 1 at full size: the reference's own corpus generator
+    (bbmh_synth_classification, SURVEY Appendix B) -> 20,000 docs x ~3,700 ids;
+    our GPU bbmh_sketch_file must reproduce the reference's sketch files
+    byte-for-byte (sha256 recorded in golden.json from the reference)."""
+    import ctypes as C
+    import hashlib
+    c1 = golden["c1"]
+    L = ref.lib
+    L.bbmh_synth_classification.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_double,
+                                            C.c_double, C.c_double, C.c_uint64, C.c_int32]
+    corpus = str(tmp_path / "c1.bbcv")
+    assert L.bbmh_synth_classification(corpus.encode(), *c1["synth"]) == 0
+    assert hashlib.sha256(open(corpus, "rb").read()).hexdigest() == c1["corpus_sha256"]
+    for scheme, digest in c1["sketch_sha256"].items():
+        f = bb.Family(int(scheme), c1["dim"], c1["k"], c1["seed"])
+        out = str(tmp_path / f"c1_{scheme}.bbmh")
+        stats = f.sketch_file(corpus, out, c1["b"], 10000, 4, False)
+        assert stats["records"] == 20000
+        assert hashlib.sha256(open(out, "rb").read()).hexdigest() == digest, scheme
