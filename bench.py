@@ -344,6 +344,19 @@ def run_ours(args):
                                          codes_out.array[: 1000 * cb]))
     h2d = n * nnz * 4 + (n + 1) * 8
     d2h = n * cb + n
+    # the e2e roofline for 2U is the PCIe H2D copy: measure pinned H2D bandwidth here
+    hb = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+    db = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    db.copy_(hb, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(3):
+        db.copy_(hb, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pcie_gbs = 3 * (1 << 30) / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del hb, db
 
     # ---- CPU baseline: the reference on this host, bounded sample (rank 0, N=1) ----
     cpu = None
@@ -388,7 +401,11 @@ def run_ours(args):
             "e2e": {"value": evals * world / e2e_s, "unit": "hash-evals/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s * 1e3, "api": "bbmh_ext_sketch_csr (pinned host CSR)",
-                    "consistent_with_device_run": e2e_consistent, "steps": args.e2e_steps},
+                    "consistent_with_device_run": e2e_consistent, "steps": args.e2e_steps,
+                    "roofline": {"bound": "pcie_h2d", "unit": "GB/s",
+                                 "achieved": h2d / e2e_s / 1e9, "peak": pcie_gbs,
+                                 "frac": h2d / e2e_s / 1e9 / pcie_gbs,
+                                 "peak_how": "pinned 1 GiB torch copy_ H2D, best of 3, this run"}},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches_kernel + e2e_launches,
