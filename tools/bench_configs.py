@@ -208,7 +208,7 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--c3-docs", type=int, default=50000)
     ap.add_argument("--c4-docs", type=int, default=677399)
-    ap.add_argument("--loader-docs", type=int, default=40000)
+    ap.add_argument("--loader-docs", type=int, default=20000)
     args = ap.parse_args()
     torch.cuda.set_device(0)
     with tempfile.TemporaryDirectory() as tmp:
