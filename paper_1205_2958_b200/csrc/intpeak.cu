@@ -26,6 +26,8 @@ enum Op : int {
     OP_VIADDMNMX = 7,  // min(x + c, x)            (alu pipe)
     OP_WIDE_XOR = 8,   // IMAD.WIDE.U32 + LOP3     (64-bit product rate)
     OP_IMAD_HI = 9,    // IMAD.HI.U32              (high-word product rate)
+    OP_WIDE_RZ = 10,   // IMAD.WIDE.U32 a, b, RZ + LOP3 (no 64-bit addend: 2 register reads)
+    OP_MIX_4U = 11,    // the 4U-bit fold step: IMAD.WIDE(+pair) + LEA.HI + VIADDMNMX
 };
 
 template <int OP>
@@ -76,8 +78,17 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
                 const uint64_t v = (uint64_t)a[i] * c1 + c2;
                 a[i] = (uint32_t)(v >> 32) ^ (uint32_t)v;
                 asm volatile("" : "+r"(a[i]));
-            } else {
+            } else if constexpr (OP == OP_IMAD_HI) {
                 asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(c1), "r"(c2));
+            } else if constexpr (OP == OP_WIDE_RZ) {
+                const uint64_t v = (uint64_t)a[i] * c1;
+                a[i] = (uint32_t)(v >> 32) ^ (uint32_t)v;
+                asm volatile("" : "+r"(a[i]));
+            } else {
+                const uint64_t v = (uint64_t)a[i] * c1 + c2;
+                const uint32_t s = (uint32_t)(v >> 32) + ((uint32_t)v >> 1);
+                a[i] = min(s, s + 0x80000001u);
+                asm volatile("" : "+r"(a[i]));
             }
         }
     }
@@ -126,6 +137,8 @@ __attribute__((visibility("default"))) double bbmh_intpeak_ops_per_thread(int op
         case OP_MIX_2U: return base * 3;  // 2 IMAD + 1 VIMNMX3
         case OP_IMAD_WIDE: return base * 2;  // IMAD.WIDE + LEA.HI
         case OP_WIDE_XOR: return base * 2;   // IMAD.WIDE + LOP3
+        case OP_WIDE_RZ: return base * 2;    // IMAD.WIDE (RZ addend) + LOP3
+        case OP_MIX_4U: return base * 3;     // IMAD.WIDE + LEA.HI + VIADDMNMX
         default: return base;
     }
 }
@@ -154,6 +167,8 @@ __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, 
         case OP_VIADDMNMX: ms = run<OP_VIADDMNMX>(blocks, threads, sink, cyc, clk, st); break;
         case OP_WIDE_XOR: ms = run<OP_WIDE_XOR>(blocks, threads, sink, cyc, clk, st); break;
         case OP_IMAD_HI: ms = run<OP_IMAD_HI>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_WIDE_RZ: ms = run<OP_WIDE_RZ>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_4U: ms = run<OP_MIX_4U>(blocks, threads, sink, cyc, clk, st); break;
         default: return -2;
     }
     unsigned long long* h = new unsigned long long[blocks];

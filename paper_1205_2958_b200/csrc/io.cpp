@@ -16,6 +16,9 @@
 #include "io.hpp"
 
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cerrno>
@@ -60,54 +63,132 @@ void read_exact(FILE* f, void* p, size_t n) {
 }
 
 // ---- BBCV ------------------------------------------------------------------
+// The file is mapped read-only. fill() walks record headers sequentially
+// (label check, bounds) -- cheap, one touch per record -- then copies and
+// validates the id runs of the batch in parallel straight into the batch's
+// page-locked buffer. The first failing record (lowest index) wins, with the
+// reference's messages (dataio.cpp:211-230).
 class BinaryReader : public CorpusReader {
 public:
-    explicit BinaryReader(const std::string& path) : path_(path) {
-        f_ = open_or_fail(path, "rb");
-        std::setvbuf(f_, nullptr, _IOFBF, 1 << 22);
+    BinaryReader(const std::string& path, unsigned threads)
+        : path_(path), threads_(std::max(1u, std::min(threads, 64u))) {
+        FILE* f = open_or_fail(path, "rb");
         uint8_t head[21];
-        read_exact(f_, head, 4);
-        if (std::memcmp(head, "BBCV", 4) != 0)
+        read_exact(f, head, 4);
+        if (std::memcmp(head, "BBCV", 4) != 0) {
+            std::fclose(f);
             fail(Errc::MalformedLine, path_ + ": not a BBCV corpus");
-        read_exact(f_, head + 4, 1);
-        if (head[4] != 1) fail(Errc::MalformedLine, path_ + ": unknown BBCV version");
-        read_exact(f_, head + 5, 16);
+        }
+        try {
+            read_exact(f, head + 4, 1);
+            if (head[4] != 1) fail(Errc::MalformedLine, path_ + ": unknown BBCV version");
+            read_exact(f, head + 5, 16);
+        } catch (...) {
+            std::fclose(f);
+            throw;
+        }
+        std::fseek(f, 0, SEEK_END);
+        size_ = uint64_t(std::ftell(f));
+        std::fclose(f);
         dim_ = get_u64(head + 5);
         count_ = get_u64(head + 13);
+        pos_ = 21;
+        fd_ = ::open(path.c_str(), O_RDONLY);
+        if (fd_ < 0) fail(Errc::Io, path_ + ": " + std::strerror(errno));
+        if (size_ > 0) {
+            void* m = ::mmap(nullptr, size_, PROT_READ, MAP_PRIVATE, fd_, 0);
+            if (m == MAP_FAILED) fail(Errc::Io, path_ + ": mmap failed");
+            map_ = static_cast<const uint8_t*>(m);
+            ::madvise(m, size_, MADV_SEQUENTIAL);
+        }
     }
     ~BinaryReader() override {
-        if (f_) std::fclose(f_);
+        if (map_) ::munmap(const_cast<uint8_t*>(map_), size_);
+        if (fd_ >= 0) ::close(fd_);
     }
 
     bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) override {
-        bool any = false;
-        while (read_ < count_ && b.n < max_docs && (b.nids() < max_ids || b.n == 0)) {
-            uint8_t h[5];
-            read_exact(f_, h, 1);
-            const int8_t label = int8_t(h[0]);
-            if (label != 1 && label != -1)
-                fail(Errc::NonBinaryLabel, "record " + std::to_string(read_) + ": bad label");
-            read_exact(f_, h + 1, 4);
-            const uint32_t n = get_u32(h + 1);
-            const uint64_t base = b.nids();
-            if (base + n > b.cap_ids) b.reserve_ids(std::max<uint64_t>(base + n, max_ids + max_ids / 4));
-            uint32_t* dst = b.ids + base;
-            read_exact(f_, dst, size_t(n) * 4);
-            uint32_t bad = 0;
-            for (uint32_t i = 1; i < n; ++i) bad |= dst[i] <= dst[i - 1];
-            if (bad) fail(Errc::NonAscendingIndex, "record " + std::to_string(read_));
-            b.row_ptr.push_back(base + n);
+        // 1. sequential header walk
+        struct Rec {
+            uint64_t src;  // byte offset of the first id
+            uint64_t dst;  // id offset in the batch
+            uint32_t n;
+        };
+        std::vector<Rec> recs;
+        Errc pend_code = Errc::Io;
+        std::string pend_msg;
+        bool pending = false;
+        uint64_t nid = b.nids();
+        const uint64_t first = read_;
+        while (read_ < count_ && b.n + recs.size() < max_docs && (nid < max_ids || recs.empty())) {
+            if (pos_ + 1 > size_) {
+                pending = true, pend_code = Errc::Io, pend_msg = "short read";
+                break;
+            }
+            const int8_t label = int8_t(map_[pos_]);
+            if (label != 1 && label != -1) {
+                pending = true, pend_code = Errc::NonBinaryLabel;
+                pend_msg = "record " + std::to_string(read_) + ": bad label";
+                break;
+            }
+            if (pos_ + 5 > size_) {
+                pending = true, pend_code = Errc::Io, pend_msg = "short read";
+                break;
+            }
+            const uint32_t n = get_u32(map_ + pos_ + 1);
+            if (pos_ + 5 + uint64_t(n) * 4 > size_) {
+                pending = true, pend_code = Errc::Io, pend_msg = "short read";
+                break;
+            }
+            recs.push_back({pos_ + 5, nid, n});
             b.labels.push_back(label);
-            ++b.n;
+            nid += n;
+            pos_ += 5 + uint64_t(n) * 4;
             ++read_;
-            any = true;
         }
-        return any;
+        if (recs.empty() && !pending) return false;
+        if (nid > b.cap_ids) b.reserve_ids(std::max<uint64_t>(nid, max_ids + max_ids / 4));
+        // 2. parallel copy + strictly-ascending check
+        const size_t nr = recs.size();
+        const unsigned W = nr < 256 ? 1u : threads_;
+        std::vector<uint64_t> bad(W, UINT64_MAX);
+        auto work = [&](unsigned w) {
+            const size_t lo = nr * w / W, hi = nr * (w + 1) / W;
+            for (size_t r = lo; r < hi; ++r) {
+                const Rec& rc = recs[r];
+                uint32_t* dst = b.ids + rc.dst;
+                std::memcpy(dst, map_ + rc.src, size_t(rc.n) * 4);
+                uint32_t nonasc = 0;
+                for (uint32_t i = 1; i < rc.n; ++i) nonasc |= dst[i] <= dst[i - 1];
+                if (nonasc) {
+                    bad[w] = r;
+                    return;
+                }
+            }
+        };
+        if (W == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> ts;
+            for (unsigned w = 1; w < W; ++w) ts.emplace_back(work, w);
+            work(0);
+            for (auto& t : ts) t.join();
+        }
+        for (unsigned w = 0; w < W; ++w)
+            if (bad[w] != UINT64_MAX)
+                fail(Errc::NonAscendingIndex, "record " + std::to_string(first + bad[w]));
+        if (pending) fail(pend_code, pend_msg);
+        for (const Rec& rc : recs) b.row_ptr.push_back(rc.dst + rc.n);
+        b.n += nr;
+        return true;
     }
 
 private:
     std::string path_;
-    FILE* f_ = nullptr;
+    unsigned threads_;
+    int fd_ = -1;
+    const uint8_t* map_ = nullptr;
+    uint64_t size_ = 0, pos_ = 0;
     uint64_t dim_ = 0, count_ = 0, read_ = 0;
 };
 
@@ -341,7 +422,8 @@ std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned pars
     char magic[4] = {0, 0, 0, 0};
     const size_t got = std::fread(magic, 1, 4, f);
     std::fclose(f);
-    if (got == 4 && std::memcmp(magic, "BBCV", 4) == 0) return std::make_unique<BinaryReader>(path);
+    if (got == 4 && std::memcmp(magic, "BBCV", 4) == 0)
+        return std::make_unique<BinaryReader>(path, parse_threads);
     return std::make_unique<LibsvmReader>(path, parse_threads);
 }
 

@@ -470,6 +470,9 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
                 return dispatch_j<S_4UMOD, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             return dispatch_j<S_4UMOD, false>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         default:
+            if (perm_tablewise_applies(F, n))  // L2-resident table-outer schedule (perm.cu)
+                return launch_perm_tablewise(F, row_ptr, base, idx, n, b, codes, minima, flags,
+                                             err, st);
             return dispatch_j<S_PERM, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
     }
 }

@@ -43,6 +43,12 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t inde
                    const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
                    uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
 
+// Permutation mode with tables too large for L2: table-outer passes (perm.cu).
+bool perm_tablewise_applies(const KernelFamily& F, uint64_t n);
+void launch_perm_tablewise(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
+                           const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
+                           uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
+
 uint64_t kernel_launch_count();
 void count_launches(uint64_t n);
 

@@ -110,6 +110,35 @@ private:
     bool total_known_ = false, aborted_ = false;
 };
 
+// Page-locked batch buffers are expensive to allocate (cudaMallocHost of
+// ~80 MB each), so they are pooled process-wide and leased per call.
+std::mutex g_batch_mu;
+std::vector<std::unique_ptr<Batch>> g_batch_pool;
+
+struct BatchLease {
+    std::vector<Batch*> batches;
+    std::vector<std::unique_ptr<Batch>> owned;
+    explicit BatchLease(size_t n) {
+        std::lock_guard lk(g_batch_mu);
+        while (owned.size() < n) {
+            if (!g_batch_pool.empty()) {
+                owned.push_back(std::move(g_batch_pool.back()));
+                g_batch_pool.pop_back();
+            } else {
+                owned.push_back(std::make_unique<Batch>());
+            }
+            batches.push_back(owned.back().get());
+        }
+    }
+    ~BatchLease() {
+        std::lock_guard lk(g_batch_mu);
+        for (auto& b : owned) {
+            b->clear();
+            g_batch_pool.push_back(std::move(b));
+        }
+    }
+};
+
 // SketchWriter (sketch.cpp:102-141): header now, count patched on close/destruction
 class SketchWriter {
 public:
@@ -177,12 +206,9 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
     const bool b_ok = b >= 1 && b <= 32;
 
     const size_t nbatches = 3 * devs.size() + 3;
-    std::vector<std::unique_ptr<Batch>> storage;
+    BatchLease storage(nbatches);  // pinned batches reused across calls
     BlockingQueue<Batch*> free_q, in_q;
-    for (size_t i = 0; i < nbatches; ++i) {
-        storage.push_back(std::make_unique<Batch>());
-        free_q.push(storage.back().get());
-    }
+    for (Batch* bt : storage.batches) free_q.push(bt);
     Reorder done;
     std::mutex err_mu;
     std::exception_ptr error;
