@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
                 __syncthreads();
             }
             const uint4* b4 = reinterpret_cast<const uint4*>(buf);
-#pragma unroll 2
+#pragma unroll(J >= 8 ? 2 : 4)
             for (uint32_t q = 0; q < n4; ++q) {
                 const uint4 t4 = b4[q];
 #pragma unroll
@@ -409,7 +409,8 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
         case 1: return launch_one<SCHEME, POW2, 1>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         case 2: return launch_one<SCHEME, POW2, 2>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         case 4: return launch_one<SCHEME, POW2, 4>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
-        default: return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case 8: return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        default: return launch_one<SCHEME, POW2, 16>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
     }
 }
 
