@@ -183,12 +183,20 @@ def roofline_int(scheme, dim, evals_per_s, sm_mhz, peaks):
     alu_rate = ops["vimnmx3"]["inst_per_clk_per_sm"]
     evals_per_clk = min(fma_rate / fma, alu_rate / alu)
     peak = 148 * evals_per_clk * sm_mhz * 1e6
-    return {"bound": "int", "unit": "Gevals/s", "achieved": evals_per_s / 1e9,
-            "peak": peak / 1e9, "frac": evals_per_s / peak,
-            "slots_per_eval": {"fma_heavy": round(fma, 3), "alu": alu},
-            "pipe_rates_per_sm_clk": {"fma_heavy": fma_rate, "alu": alu_rate},
-            "binding_pipe": "fma_heavy" if fma_rate / fma <= alu_rate / alu else "alu",
-            "sm_mhz": sm_mhz, "peaks": "measured by tools/intpeak.py in this run"}
+    out = {"bound": "int", "unit": "Gevals/s", "achieved": evals_per_s / 1e9,
+           "peak": peak / 1e9, "frac": evals_per_s / peak,
+           "slots_per_eval": {"fma_heavy": round(fma, 3), "alu": alu},
+           "pipe_rates_per_sm_clk": {"fma_heavy": fma_rate, "alu": alu_rate},
+           "binding_pipe": "fma_heavy" if fma_rate / fma <= alu_rate / alu else "alu",
+           "sm_mhz": sm_mhz, "peaks": "measured by tools/intpeak.py in this run"}
+    mix = ops.get("mix_2u_reuse(2imad:1vimnmx3)")
+    if scheme == "2u" and mix and mix.get("inst_per_clk_per_sm"):
+        # the same 2 IMAD : 1 VIMNMX3 mix with no memory or loop control reaches
+        # only this fraction of the IMAD pipe: the practical ceiling of the loop
+        ceil = mix["inst_per_clk_per_sm"] * 2 / 3 / fma_rate
+        out["mix_ceiling_frac"] = ceil
+        out["frac_of_mix_ceiling"] = out["frac"] / ceil
+    return out
 
 
 # ---- the two arms -----------------------------------------------------------------

@@ -67,6 +67,7 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
     kf.dim_pow2 = f.dim_pow2 ? 1 : 0;
     kf.dim_mask = uint32_t(f.dim - 1);
     kf.dim32 = uint32_t(f.dim);
+    kf.neg_dim32 = 0u - uint32_t(f.dim);
     kf.p = uint32_t(f.p);
     kf.barrett = f.p ? (~0ull) / f.p : 0;
     if (f.scheme == Scheme::FourUBit || f.scheme == Scheme::FourUMod) {

@@ -55,7 +55,7 @@ __device__ __forceinline__ uint32_t m31_fold(uint32_t h, uint32_t t2, uint32_t c
 // x mod p for x < 2^62, 3 <= p < 2^31 (and p = 2), barrett = floor((2^64-1)/p)
 __device__ __forceinline__ uint32_t mod_barrett(uint64_t x, uint32_t p, uint64_t barrett) {
     const uint64_t q = __umul64hi(x, barrett);
-    const uint32_t r = (uint32_t)x - (uint32_t)q * p;  // true r in [0, 2p)
+    const uint32_t r = (uint32_t)x + (uint32_t)q * (0u - p);  // x - q*p; true r in [0, 2p)
     return min(r, r - p);
 }
 
@@ -64,7 +64,8 @@ __device__ __forceinline__ uint32_t reduce_dim(const KernelFamily& F, uint32_t h
     if constexpr (POW2) {
         return h & F.dim_mask;
     } else {
-        return h - F.dim32 * (__umulhi(h, F.magic) >> F.magic_shift);
+        // h - D*q as h + q*(2^32 - D): one IMAD, no negation (IMAD.MOV) on the fma pipe
+        return h + F.neg_dim32 * (__umulhi(h, F.magic) >> F.magic_shift);
     }
 }
 

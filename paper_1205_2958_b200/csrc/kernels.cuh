@@ -18,6 +18,7 @@ struct KernelFamily {
     uint32_t dim_mask = 0;   // 4U: dim - 1 when dim is a power of two
     uint32_t dim_pow2 = 1;
     uint32_t dim32 = 0;      // 4U: dim (< 2^31) for the magic-division branch
+    uint32_t neg_dim32 = 0;  // 2^32 - dim32 (h - q*D computed as h + q*neg_dim32)
     uint32_t magic = 0;      // 4U: h % dim = h - dim * (umulhi(h, magic) >> magic_shift)
     uint32_t magic_shift = 0;
     uint32_t p = 0;          // 4U modulus
