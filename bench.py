@@ -389,8 +389,17 @@ def run_ours(args):
     pin.free()
     codes_out.free()
 
+    traffic = {}
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath) and n == N_DOCS:
+        # dram__bytes_read.sum + dram__bytes_write.sum of one full-size 2U launch
+        # from the committed `ncu --set full` capture (tools/gpu_ncu_full.sh)
+        traffic = json.load(open(tpath)).get("2u", {})
     if rank == 0:
         head = results["2u"]
+        if head.get("roofline") is not None:
+            head["roofline"]["traffic"] = traffic.get("dram_bytes_per_launch")
+            head["roofline"]["traffic_source"] = traffic.get("source")
         line = {
             "metric": "hash_evals_per_sec", "value": head["hash_evals_per_sec"],
             "unit": "hash-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -404,7 +413,8 @@ def run_ours(args):
             "roofline": head.get("roofline"),
             "roofline_hbm": {"bound": "hbm", "unit": "GB/s", "achieved": head.get("hbm_gbs_algorithmic"),
                              "peak": 6461.2, "frac": (head.get("hbm_gbs_algorithmic") or 0) / 6461.2,
-                             "traffic": None},
+                             "traffic": traffic.get("dram_bytes_per_launch"),
+                             "algorithmic_bytes_per_launch": n * nnz * 4 + (n + 1) * 8 + n * cb + n},
             "schemes": results,
             "e2e": {"value": evals * world / e2e_s, "unit": "hash-evals/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
