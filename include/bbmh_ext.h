@@ -38,6 +38,28 @@ BBMH_API bbmh_status bbmh_ext_sketch_csr_device(const bbmh_family* family,
                                                 uint64_t* d_minima, uint8_t* d_flags,
                                                 void* stream);
 
+/* Fused test-time scoring (the reference's prediction on a sketch, run
+ * without materialising the sketch or its expansion): each row is sketched
+ * and scored on the GPU against a linear model over the k*2^b expansion,
+ *   scores_out[r] = sum_{j ascending} weights[j*2^b + code_j]
+ * in double precision and in the reference's summation order
+ * (predict_score, proj/src/learner.cpp:510-521); rows with no ids score 0
+ * (learner.cpp:528). An expanded index >= weights_dim fails with
+ * BBMH_E_DIMENSION_EXCEEDED "feature <idx> >= dim <dim>" (learner.cpp:515). */
+BBMH_API bbmh_status bbmh_ext_sketch_score_csr(const bbmh_family* family, const uint64_t* row_ptr,
+                                               const uint32_t* indices, uint64_t n, uint32_t b,
+                                               const double* weights, uint64_t weights_dim,
+                                               double* scores_out);
+
+/* File form: corpus (LibSVM text or BBCV) + BBLM model -> "%d\t%.9g\n" per
+ * row and the accuracy, byte-identical to bbmh_sketch_file followed by
+ * bbmh_predict on the resulting sketch (proj/src/capi.cpp:307-317).
+ * scores_path may be NULL/"" (no table) or "-" (stdout). */
+BBMH_API bbmh_status bbmh_ext_predict_corpus(const bbmh_family* family, uint32_t b,
+                                             const char* model_path, const char* corpus_path,
+                                             const char* scores_path, uint32_t workers,
+                                             double* accuracy_out);
+
 /* Device list used by bbmh_ext_sketch_csr and bbmh_sketch_file (default:
  * the current device only). Chunks are assigned dynamically; output order
  * and bytes do not depend on the device count. */

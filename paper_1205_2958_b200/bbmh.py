@@ -86,6 +86,11 @@ def lib() -> C.CDLL:
         "bbmh_ext_sketch_csr_device": ([C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
                                         C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_void_p], C.c_int32),
+        "bbmh_ext_sketch_score_csr": ([C.c_void_p, u64p, u32p, C.c_uint64, C.c_uint32,
+                                       C.POINTER(C.c_double), C.c_uint64,
+                                       C.POINTER(C.c_double)], C.c_int32),
+        "bbmh_ext_predict_corpus": ([C.c_void_p, C.c_uint32, C.c_char_p, C.c_char_p, C.c_char_p,
+                                     C.c_uint32, C.POINTER(C.c_double)], C.c_int32),
         "bbmh_ext_set_devices": ([i32p, C.c_uint32], C.c_int32),
         "bbmh_ext_get_devices": ([i32p, C.c_uint32, C.POINTER(C.c_uint32)], C.c_int32),
         "bbmh_ext_family_prepare": ([C.c_void_p, C.c_int32], C.c_int32),
@@ -204,6 +209,29 @@ class Family:
         """bbmh_ext_sketch_csr_device; arguments are raw device pointers (ints)."""
         _check(lib().bbmh_ext_sketch_csr_device(self.handle, d_row_ptr, index_base, d_indices, n,
                                                 b, d_codes, d_minima, d_flags, stream))
+
+    def sketch_score_csr(self, row_ptr, indices, b: int, weights):
+        """bbmh_ext_sketch_score_csr: fused sketch + linear score per row (float64[n])."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+        idx = np.ascontiguousarray(indices, dtype=np.uint32)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        n = rp.size - 1
+        scores = np.empty(n, np.float64)
+        _check(lib().bbmh_ext_sketch_score_csr(
+            self.handle, _ptr(rp, u64p), _ptr(idx, u32p) if idx.size else None, n, b,
+            _ptr(w, C.POINTER(C.c_double)) if w.size else None, w.size,
+            _ptr(scores, C.POINTER(C.c_double))))
+        return scores
+
+    def predict_corpus(self, b: int, model_path, corpus_path, scores_path=None,
+                       workers: int = 1) -> float:
+        """bbmh_ext_predict_corpus: corpus + BBLM model -> scores table; returns accuracy."""
+        acc = C.c_double(0)
+        _check(lib().bbmh_ext_predict_corpus(
+            self.handle, b, None if model_path is None else os.fsencode(model_path),
+            None if corpus_path is None else os.fsencode(corpus_path),
+            None if scores_path is None else os.fsencode(scores_path), workers, C.byref(acc)))
+        return acc.value
 
     def sketch_file(self, input_path, output_path, b: int, chunk_size: int = 10000,
                     workers: int = 1, emit_minima: bool = False) -> dict:

@@ -217,6 +217,38 @@ bbmh_status bbmh_ext_sketch_csr_device(const bbmh_family* family, const uint64_t
     });
 }
 
+bbmh_status bbmh_ext_sketch_score_csr(const bbmh_family* family, const uint64_t* row_ptr,
+                                      const uint32_t* indices, uint64_t n, uint32_t b,
+                                      const double* weights, uint64_t weights_dim,
+                                      double* scores_out) {
+    return guarded([&] {
+        if (!family || !scores_out) fail(Errc::InvalidArgument, "family and scores_out required");
+        if (n > 0 && !row_ptr) fail(Errc::InvalidArgument, "row_ptr must not be NULL");
+        if (weights_dim > 0 && !weights) fail(Errc::InvalidArgument, "weights must not be NULL");
+        const uint32_t b8 = narrow_b(b);
+        if (n == 0) return;
+        if (row_ptr[n] > row_ptr[0] && !indices)
+            fail(Errc::InvalidArgument, "indices must not be NULL");
+        static const uint32_t kNone = 0;
+        ScoreModel model{weights, weights_dim};
+        sketch_rows_host(*family->impl, row_ptr, indices ? indices : &kNone, n, b8, nullptr,
+                         nullptr, nullptr, &model, scores_out);
+    });
+}
+
+bbmh_status bbmh_ext_predict_corpus(const bbmh_family* family, uint32_t b, const char* model_path,
+                                    const char* corpus_path, const char* scores_path,
+                                    uint32_t workers, double* accuracy_out) {
+    return guarded([&] {
+        if (!family) fail(Errc::InvalidArgument, "family must not be NULL");
+        const char* model = require(model_path, "model_path");
+        const char* data = require(corpus_path, "corpus_path");
+        if (workers < 1) fail(Errc::InvalidArgument, "workers must be >= 1");
+        predict_file(*family->impl, uint8_t(b), model, data, scores_path ? scores_path : "",
+                     workers, accuracy_out);
+    });
+}
+
 bbmh_status bbmh_ext_set_devices(const int32_t* ids, uint32_t count) {
     return guarded([&] {
         if (count && !ids) fail(Errc::InvalidArgument, "ids must not be NULL");

@@ -242,16 +242,30 @@ void set_chunk_docs(uint64_t docs) {
 }
 
 // ---- Lane ------------------------------------------------------------------
-Lane::Lane(const Family& f, int device, uint32_t b, bool want_minima)
+Lane::Lane(const Family& f, int device, uint32_t b, bool want_minima, const ScoreModel* score)
     : f_(f), device_(device), b_(b), cb_(packed_code_bytes(f.k, b)), want_minima_(want_minima) {
     df_ = &device_family(f, device);
     for (int i = 0; i < kSlots; ++i) slots_[i] = acquire_slot(device);
+    if (score) {
+        DeviceGuard g(device);
+        wdim_ = score->dim;
+        BBMH_CUDA(cudaMalloc(&d_w_, std::max<uint64_t>(wdim_, 1) * sizeof(double)));
+        if (wdim_)
+            BBMH_CUDA(cudaMemcpy(d_w_, score->w, wdim_ * sizeof(double), cudaMemcpyHostToDevice));
+    }
 }
 
 Lane::~Lane() {
     for (int i = 0; i < kSlots; ++i) {
         if (slots_[i] && slots_[i]->busy) cudaStreamSynchronize(slots_[i]->st);
         release_slot(slots_[i]);
+    }
+    if (d_w_) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device_);
+        cudaFree(d_w_);
+        cudaSetDevice(prev);
     }
 }
 
@@ -286,6 +300,18 @@ void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) 
             s.cap_min = std::min(c1, c2);
         }
     }
+    if (d_w_) {
+        if (!s.d_bad) {
+            BBMH_CUDA(cudaMalloc(&s.d_bad, sizeof(unsigned long long)));
+            BBMH_CUDA(cudaMallocHost(&s.h_bad, sizeof(unsigned long long)));
+        }
+        if (rows > s.cap_scores) {
+            uint64_t c1 = s.cap_scores, c2 = s.cap_scores;
+            grow_device(s.d_scores, c1, std::max<uint64_t>(rows, 1));
+            grow_host(s.h_scores, c2, std::max<uint64_t>(rows, 1));
+            s.cap_scores = std::min(c1, c2);
+        }
+    }
 }
 
 void Lane::enqueue(Slot& s, const ChunkJob& job) {
@@ -312,6 +338,15 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
     launch_sketch(df_->kf, s.d_rp, job.index_base, s.d_idx, n, b_, s.d_codes,
                   want_minima_ ? s.d_min : nullptr, s.d_flags, s.d_err, s.st);
     BBMH_CUDA(cudaGetLastError());
+    if (d_w_) {  // fused scoring on the device-resident codes (score.cu)
+        BBMH_CUDA(cudaMemsetAsync(s.d_bad, 0xff, sizeof(unsigned long long), s.st));
+        launch_score(s.d_codes, s.d_flags, n, f_.k, b_, d_w_, wdim_, s.d_scores, s.d_bad, s.st);
+        BBMH_CUDA(cudaGetLastError());
+        BBMH_CUDA(cudaMemcpyAsync(s.h_scores, s.d_scores, n * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s.st));
+        BBMH_CUDA(cudaMemcpyAsync(s.h_bad, s.d_bad, sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s.st));
+    }
     BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
     if (n && cb_)
         BBMH_CUDA(cudaMemcpyAsync(s.h_codes, s.d_codes, n * cb_, cudaMemcpyDeviceToHost, s.st));
@@ -336,13 +371,30 @@ ChunkResult Lane::finish(Slot& s) {
     r.codes = s.h_codes;
     r.minima = want_minima_ ? s.h_min : nullptr;
     r.flags = s.h_flags;
+    if (d_w_) {
+        if (*s.h_bad != ~0ull) {  // predict_score (learner.cpp:515-517), first offender in order
+            const uint64_t row = *s.h_bad >> 24;
+            const uint32_t j = uint32_t(*s.h_bad & 0xffffff);
+            const uint8_t* c = s.h_codes + row * cb_;
+            uint32_t code = 0;
+            for (uint32_t i = 0; i < b_; ++i) {
+                const uint64_t pos = uint64_t(j) * b_ + i;
+                code |= uint32_t((c[pos >> 3] >> (pos & 7)) & 1u) << i;
+            }
+            const uint32_t idx = uint32_t((uint64_t(j) << b_) + code);
+            fail(Errc::DimensionExceeded,
+                 "feature " + std::to_string(idx) + " >= dim " + std::to_string(wdim_));
+        }
+        r.scores = s.h_scores;
+    }
     cudaEventElapsedTime(&r.kernel_ms, s.ev0, s.ev1);
     return r;
 }
 
 // ---- host-buffer CSR entry -------------------------------------------------
 void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* indices,
-                      uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima, uint8_t* flags) {
+                      uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima, uint8_t* flags,
+                      const ScoreModel* score, double* scores) {
     if (n == 0) return;
     check_row_ptr(row_ptr, n);
     const size_t cb = packed_code_bytes(f.k, b);
@@ -367,10 +419,11 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
 
     auto run_device = [&](int dev) {
         try {
-            Lane lane(f, dev, b, minima != nullptr);
+            Lane lane(f, dev, b, minima != nullptr, score);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
-                std::memcpy(codes + r0 * cb, res.codes, res.n * cb);
+                if (codes) std::memcpy(codes + r0 * cb, res.codes, res.n * cb);
+                if (scores) std::memcpy(scores + r0, res.scores, res.n * sizeof(double));
                 if (minima) std::memcpy(minima + r0 * f.k, res.minima, res.n * f.k * 8);
                 if (flags) std::memcpy(flags + r0, res.flags, res.n);
             };

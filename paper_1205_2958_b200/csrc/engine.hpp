@@ -34,9 +34,13 @@ void set_pipeline_devices(const std::vector<int>& ids);
 uint64_t chunk_docs_setting();
 void set_chunk_docs(uint64_t docs);
 
-// Host buffers in, host buffers out; synchronous. Validates row_ptr.
+struct ScoreModel;
+
+// Host buffers in, host buffers out; synchronous. Validates row_ptr. With a
+// score model the rows are also scored on the device (codes may then be null).
 void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* indices,
-                      uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima, uint8_t* flags);
+                      uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima, uint8_t* flags,
+                      const ScoreModel* score = nullptr, double* scores = nullptr);
 
 // Device buffers on the current device; asynchronous on `stream`.
 void sketch_rows_device(const Family& f, const uint64_t* d_row_ptr, uint64_t index_base,
@@ -62,13 +66,22 @@ struct ChunkResult {
     const uint8_t* codes = nullptr;    // pinned, n * cb
     const uint64_t* minima = nullptr;  // pinned, n * k (or null)
     const uint8_t* flags = nullptr;    // pinned, n
+    const double* scores = nullptr;    // pinned, n (scoring lanes only)
     float kernel_ms = 0;               // device time of the sketch kernel
+};
+
+// Linear model over the k*2^b expansion for the fused scoring path
+// (learner.cpp:510-521): scores[r] = sum_j w[j*2^b + code_j].
+struct ScoreModel {
+    const double* w = nullptr;  // host, dim doubles
+    uint64_t dim = 0;
 };
 
 class Lane {
 public:
     static constexpr int kSlots = 3;
-    Lane(const Family& f, int device, uint32_t b, bool want_minima);
+    Lane(const Family& f, int device, uint32_t b, bool want_minima,
+         const ScoreModel* score = nullptr);
     ~Lane();
     Lane(const Lane&) = delete;
     Lane& operator=(const Lane&) = delete;
@@ -106,6 +119,11 @@ public:
         uint64_t* h_min = nullptr;
         uint8_t* h_flags = nullptr;
         int* h_err = nullptr;
+        double* d_scores = nullptr;
+        double* h_scores = nullptr;
+        unsigned long long* d_bad = nullptr;
+        unsigned long long* h_bad = nullptr;
+        uint64_t cap_scores = 0;
         uint64_t cap_rows = 0, cap_idx = 0, cap_idx_pinned = 0, cap_codes = 0, cap_min = 0;
         bool busy = false;
         ChunkJob job;
@@ -122,6 +140,8 @@ private:
     uint32_t b_;
     size_t cb_;
     bool want_minima_;
+    double* d_w_ = nullptr;  // device copy of the scoring model (owned by the lane)
+    uint64_t wdim_ = 0;
     uint64_t next_ = 0;
     Slot* slots_[kSlots] = {};
 };

@@ -50,6 +50,13 @@ void launch_perm_tablewise(const KernelFamily& F, const uint64_t* row_ptr, uint6
                            const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
                            uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
 
+// Fused scoring of freshly sketched rows against a linear model over the
+// k*2^b expansion (score.cu). `bad` receives min(row << 24 | j) of the first
+// index >= wdim (initialise to ~0).
+void launch_score(const uint8_t* codes, const uint8_t* flags, uint64_t n, uint32_t k, uint32_t b,
+                  const double* w, uint64_t wdim, double* scores, unsigned long long* bad,
+                  cudaStream_t stream);
+
 uint64_t kernel_launch_count();
 void count_launches(uint64_t n);
 

@@ -70,6 +70,7 @@ struct OutBatch {
     uint64_t n = 0;
     std::vector<uint8_t> recs;     // n * (2 + cb): label, flags, codes
     std::vector<uint64_t> minima;  // n * k (optional)
+    std::vector<double> scores;    // n (scoring pipeline only)
 };
 
 // order-restoring buffer (pipeline.cpp:77-119)
@@ -187,18 +188,12 @@ private:
     uint64_t count_ = 0;
 };
 
-}  // namespace
 
-PipelineStats sketch_file(const Family& f, const std::string& input_path,
-                          const std::string& output_path, uint8_t b, uint64_t chunk_size,
-                          uint32_t workers, bool emit_minima) {
-    const auto wall0 = Clock::now();
-    // open order as in sketch_file (pipeline.cpp:217-220) and sketch_stream (:125-126)
-    auto reader = open_corpus(input_path, workers ? workers : 1);
-    SketchWriter writer(output_path, f, b, emit_minima);
-    if (chunk_size < 1) fail(Errc::InvalidArgument, "chunk_size must be >= 1");
-    if (workers < 1) fail(Errc::InvalidArgument, "workers must be >= 1");
-
+// Shared engine of the file pipelines: reader thread -> pinned batches ->
+// one lane per GPU -> `append(OutBatch)` on the calling thread, in order.
+template <typename Append>
+PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool emit_minima,
+                         const ScoreModel* score, Append&& append) {
     PipelineStats stats;
     const size_t cb = packed_code_bytes(f.k, b);
     const std::vector<int> devs = pipeline_devices();
@@ -232,7 +227,7 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
                 const auto t0 = Clock::now();
                 bt->clear();
                 bt->reserve_ids(kBatchIds + kBatchIds / 4);
-                const bool got = reader->fill(*bt, max_docs, kBatchIds);
+                const bool got = reader.fill(*bt, max_docs, kBatchIds);
                 read_s += since(t0);
                 if (!got) break;
                 if (!b_ok) fail(Errc::InvalidArgument, "b must be in 1..32");  // sketch.cpp:73
@@ -256,7 +251,7 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
         lanes.emplace_back([&, di] {
             try {
                 BBMH_CUDA(cudaSetDevice(devs[di]));
-                Lane lane(f, devs[di], b_ok ? b : 8, emit_minima);
+                Lane lane(f, devs[di], b_ok ? b : 8, emit_minima, score);
                 std::map<uint64_t, Batch*> inflight;
                 auto on_done = [&](const ChunkResult& r) {
                     Batch* bt = inflight.at(r.tag);
@@ -271,6 +266,7 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
                         std::memcpy(p + 2, r.codes + i * cb, cb);
                     }
                     if (emit_minima) ob.minima.assign(r.minima, r.minima + r.n * f.k);
+                    if (r.scores) ob.scores.assign(r.scores, r.scores + r.n);
                     kernel_ms[di] += r.kernel_ms;
                     const uint64_t seq = bt->seq;
                     free_q.push(bt);
@@ -300,7 +296,7 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
         OutBatch ob;
         for (uint64_t seq = 0; done.take(seq, ob); ++seq) {
             const auto t0 = Clock::now();
-            writer.append(ob);
+            append(ob);
             stats.write_seconds += since(t0);
         }
     } catch (...) {
@@ -309,10 +305,91 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
     rd.join();
     for (auto& t : lanes) t.join();
     if (error) std::rethrow_exception(error);
-    writer.close();
-
     for (double ms : kernel_ms) stats.compute_seconds += ms * 1e-3;
+    return stats;
+}
+
+}  // namespace
+
+PipelineStats sketch_file(const Family& f, const std::string& input_path,
+                          const std::string& output_path, uint8_t b, uint64_t chunk_size,
+                          uint32_t workers, bool emit_minima) {
+    const auto wall0 = Clock::now();
+    // open order as in sketch_file (pipeline.cpp:217-220) and sketch_stream (:125-126)
+    auto reader = open_corpus(input_path, workers ? workers : 1);
+    SketchWriter writer(output_path, f, b, emit_minima);
+    if (chunk_size < 1) fail(Errc::InvalidArgument, "chunk_size must be >= 1");
+    if (workers < 1) fail(Errc::InvalidArgument, "workers must be >= 1");
+    PipelineStats stats = run_stream(f, *reader, b, emit_minima, nullptr,
+                                     [&](const OutBatch& ob) { writer.append(ob); });
+    writer.close();
     stats.chunks = (stats.records + chunk_size - 1) / chunk_size;  // reference chunking
+    stats.wall_seconds = since(wall0);
+    return stats;
+}
+
+namespace {
+
+// load_model (learner.cpp:588-612): "BBLM", u64 dim, u8 loss, u8 averaging,
+// dim doubles w, [dim doubles w_avg]; decision weights = averaging ? w_avg : w
+std::vector<double> load_decision_weights(const std::string& path) {
+    FILE* fm = open_or_fail(path, "rb");
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } guard{fm};
+    auto read_exact = [&](void* p, size_t n) {
+        if (std::fread(p, 1, n, fm) != n) fail(Errc::Io, "short read");
+    };
+    char magic[4];
+    if (std::fread(magic, 1, 4, fm) != 4 || std::memcmp(magic, "BBLM", 4) != 0)
+        fail(Errc::MalformedLine, path + ": not a BBLM model file");
+    uint8_t d8[8];
+    read_exact(d8, 8);
+    const uint64_t dim = get_u64(d8);
+    uint8_t tags[2];
+    if (std::fread(tags, 1, 2, fm) != 2 || tags[0] > 1 || tags[1] > 1)
+        fail(Errc::MalformedLine, path + ": bad loss/averaging tags");
+    std::vector<double> w(dim);
+    read_exact(w.data(), dim * sizeof(double));
+    if (tags[1]) read_exact(w.data(), dim * sizeof(double));  // w_avg replaces w
+    return w;
+}
+
+}  // namespace
+
+PipelineStats predict_file(const Family& f, uint8_t b, const std::string& model_path,
+                           const std::string& corpus_path, const std::string& scores_path,
+                           uint32_t workers, double* accuracy) {
+    const auto wall0 = Clock::now();
+    // bbmh_predict order (capi.cpp:307-317): model, data, then the scores table
+    std::vector<double> w = load_decision_weights(model_path);
+    auto reader = open_corpus(corpus_path, workers ? workers : 1);
+    FILE* out = nullptr;
+    if (!scores_path.empty()) {
+        out = scores_path == "-" ? stdout : std::fopen(scores_path.c_str(), "wb");
+        if (!out) fail(Errc::Io, scores_path + ": cannot open for writing");
+    }
+    struct Closer {
+        FILE* f;
+        ~Closer() {
+            if (f && f != stdout) std::fclose(f);
+        }
+    } guard{out};
+    ScoreModel model{w.data(), w.size()};
+    uint64_t n = 0, correct = 0;
+    std::string line;
+    PipelineStats stats = run_stream(f, *reader, b, false, &model, [&](const OutBatch& ob) {
+        const size_t rb = 2 + packed_code_bytes(f.k, b);
+        for (uint64_t i = 0; i < ob.n; ++i) {  // predict_file (learner.cpp:524-536)
+            const double score = ob.scores[i];
+            const int cls = score >= 0 ? 1 : -1;
+            if (out) std::fprintf(out, "%d\t%.9g\n", cls, score);
+            correct += cls == int8_t(ob.recs[i * rb]);
+        }
+        n += ob.n;
+    });
+    if (accuracy) *accuracy = n ? double(correct) / double(n) : 0.0;
     stats.wall_seconds = since(wall0);
     return stats;
 }

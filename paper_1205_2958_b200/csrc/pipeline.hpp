@@ -24,6 +24,13 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
                           const std::string& output_path, uint8_t b, uint64_t chunk_size,
                           uint32_t workers, bool emit_minima);
 
+// Fused test-time path: corpus -> GPU sketch -> GPU score
+// against a BBLM model -> "%d\t%.9g\n" rows, exactly what sketch_file followed
+// by bbmh_predict on the sketch produces (capi.cpp:307-317, learner.cpp:524-536).
+PipelineStats predict_file(const Family& f, uint8_t b, const std::string& model_path,
+                           const std::string& corpus_path, const std::string& scores_path,
+                           uint32_t workers, double* accuracy);
+
 // expand_stream (expansion.cpp:47-90): BBMH sketch -> BBCV rows or LibSVM text.
 uint64_t expand_file(const std::string& sketch_path, const std::string& out_path, bool binary);
 
