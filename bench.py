@@ -253,8 +253,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; BBMH_BENCH_DIST_BACKEND=gloo + rank % device_count lets the
+    # N>1 path be exercised on a 1-GPU box (tests), the driver's runs use NCCL
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BBMH_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1205_2958_b200 import _build
@@ -270,7 +277,8 @@ def run_ours(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+        t = torch.tensor([x], dtype=torch.float64, device=on)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

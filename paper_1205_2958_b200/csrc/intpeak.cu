@@ -29,6 +29,7 @@ enum Op : int {
     OP_WIDE_RZ = 10,   // IMAD.WIDE.U32 a, b, RZ + LOP3 (no 64-bit addend: 2 register reads)
     OP_MIX_4U = 11,    // the 4U-bit fold step: IMAD.WIDE(+pair) + LEA.HI + VIADDMNMX
     OP_MIX_2U_REUSE = 12,  // 2 IMAD : 1 VIMNMX3 with the coefficients in fixed operand slots
+    OP_MIX_2U_CONST = 13,  // 2 IMAD : 1 VIMNMX3 with the multiplier from the constant bank
 };
 
 template <int OP>
@@ -90,6 +91,14 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
                 const uint32_t s = (uint32_t)(v >> 32) + ((uint32_t)v >> 1);
                 a[i] = min(s, s + 0x80000001u);
                 asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_MIX_2U_CONST) {
+                // multiplier straight from the kernel-parameter constant bank
+                uint32_t h0, h1;
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h0) : "r"(a[i]), "r"(seed), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(seed), "r"(c2));
+                w[i] = h0;
+                a[i] = min(min(a[i], h0), h1);
+                asm volatile("" : "+r"(a[i]));
             } else {
                 // two products with (c1, c2) in the same slots -> operand-reuse friendly
                 uint32_t h0, h1;
@@ -149,6 +158,7 @@ __attribute__((visibility("default"))) double bbmh_intpeak_ops_per_thread(int op
         case OP_WIDE_RZ: return base * 2;    // IMAD.WIDE (RZ addend) + LOP3
         case OP_MIX_4U: return base * 3;     // IMAD.WIDE + LEA.HI + VIADDMNMX
         case OP_MIX_2U_REUSE: return base * 3;
+        case OP_MIX_2U_CONST: return base * 3;
         default: return base;
     }
 }
@@ -180,6 +190,7 @@ __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, 
         case OP_WIDE_RZ: ms = run<OP_WIDE_RZ>(blocks, threads, sink, cyc, clk, st); break;
         case OP_MIX_4U: ms = run<OP_MIX_4U>(blocks, threads, sink, cyc, clk, st); break;
         case OP_MIX_2U_REUSE: ms = run<OP_MIX_2U_REUSE>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_2U_CONST: ms = run<OP_MIX_2U_CONST>(blocks, threads, sink, cyc, clk, st); break;
         default: return -2;
     }
     unsigned long long* h = new unsigned long long[blocks];
