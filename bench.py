@@ -79,6 +79,14 @@ def make_corpus_host(n, nnz, dim, seed):
     return (np.arange(n + 1, dtype=np.uint64) * nnz), ids.reshape(-1).astype(np.uint32)
 
 
+def workload_config(docs_per_gpu, world, **extra):
+    """The `config` object shared by both arms (BASELINE.json configs[1])."""
+    return {"workload": "webspam-shape C2: 350,000 docs/GPU x 3,728 nnz, 2U D=2^24, k=500, b=8",
+            "docs_per_gpu": docs_per_gpu, "nnz_per_doc": NNZ, "k": K, "b": B, "dim_2u": D_2U,
+            "dim_4u": D_WEBSPAM, "parallelism": f"doc-sharded x{world}",
+            "l2": "inputs (5.2 GB/GPU) exceed L2; no flush needed", **extra}
+
+
 # ---- clocks ----------------------------------------------------------------------
 
 class ClockSampler:
@@ -236,8 +244,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"webspam-shape {args.scheme} k={K} b={B} (bounded sample)",
-                   "docs_per_step": n_sample, "nnz_per_doc": NNZ, "dim": dim, "k": K, "b": B},
+        "config": workload_config(N_DOCS, 1, reference_sample_docs=n_sample),
         "docs_per_sec": n_sample / t,
         "cpu_baseline": {"value": v, "unit": "hash-evals/s", "cores": threads, "kind": "reference",
                          "sample": f"{n_sample} webspam-shaped docs per step (of {N_DOCS}), "
@@ -413,10 +420,7 @@ def run_ours(args):
             "unit": "hash-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform sorted ids, device-generated)",
-            "config": {"workload": "webspam-shape C2: 350,000 docs/GPU x 3,728 nnz, 2U D=2^24, k=500, b=8",
-                       "docs_per_gpu": n, "nnz_per_doc": nnz, "k": K, "b": B, "dim_2u": D_2U,
-                       "dim_4u": D_WEBSPAM, "parallelism": f"doc-sharded x{world}",
-                       "l2": "inputs (5.2 GB/GPU) exceed L2; no flush needed"},
+            "config": workload_config(n, world),
             "docs_per_sec": head["docs_per_sec"],
             "roofline": head.get("roofline"),
             "roofline_hbm": {"bound": "hbm", "unit": "GB/s", "achieved": head.get("hbm_gbs_algorithmic"),

@@ -325,8 +325,15 @@ bbmh_status bbmh_train(const char*, const char*, const char*, const char*,
                        const bbmh_train_config*) {
     return not_provided("bbmh_train");
 }
-bbmh_status bbmh_predict(const char*, const char*, const char*, double*) {
-    return not_provided("bbmh_predict");
+// capi.cpp:307-317 -> predict_file (learner.cpp:524-536), scored on the GPU
+bbmh_status bbmh_predict(const char* model_path, const char* data_path, const char* scores_path,
+                         double* accuracy_out) {
+    return guarded([&] {
+        const char* model = require(model_path, "model_path");
+        const double acc = predict_data(model, data_path,
+                                        scores_path && *scores_path ? scores_path : "", 8);
+        if (accuracy_out) *accuracy_out = acc;
+    });
 }
 bbmh_status bbmh_synth_pair(uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, const char*,
                             int32_t) {

@@ -203,10 +203,12 @@ inline bool is_value_end(char c) {
     return c == ' ' || c == '\t' || c == '\0' || c == '\r' || c == '#';
 }
 
-// parse_libsvm (dataio.cpp:60-106), binary mode with 0/1 labels accepted.
+// parse_libsvm (dataio.cpp:60-106) with 0/1 labels accepted. Binary mode
+// (vals == nullptr, the sketch loader) rejects values != 1; value mode (the
+// prediction loader, learner.cpp:254) keeps float(val) per id.
 // `line` is NUL-terminated. Appends ids; returns false with `err` set.
 bool parse_line(const char* line, uint64_t line_no, std::vector<uint32_t>& ids, int8_t& label,
-                LineErr& err) {
+                LineErr& err, std::vector<float>* vals = nullptr) {
     auto bad = [&](Errc c, const std::string& what) {
         err.code = c;
         err.msg = "line " + std::to_string(line_no) + ": " + what;
@@ -266,7 +268,9 @@ bool parse_line(const char* line, uint64_t line_no, std::vector<uint32_t>& ids, 
             if (end == p) return bad(Errc::MalformedLine, "missing value");
         }
         p = end;
-        if (val != 1.0)
+        if (vals)
+            vals->push_back(float(val));
+        else if (val != 1.0)
             return bad(Errc::NonBinaryValue, "value " + std::to_string(val) + " in binary mode");
         ids.push_back(uint32_t(idx - 1));
     }
@@ -275,8 +279,8 @@ bool parse_line(const char* line, uint64_t line_no, std::vector<uint32_t>& ids, 
 
 class LibsvmReader : public CorpusReader {
 public:
-    LibsvmReader(const std::string& path, unsigned threads)
-        : path_(path), threads_(std::max(1u, std::min(threads, 64u))) {
+    LibsvmReader(const std::string& path, unsigned threads, bool binary)
+        : path_(path), threads_(std::max(1u, std::min(threads, 64u))), binary_(binary) {
         f_ = open_or_fail(path, "rb");
         buf_.resize(kBlock + 1);
     }
@@ -350,6 +354,7 @@ private:
 
     struct Frag {
         std::vector<uint32_t> ids;
+        std::vector<float> vals;
         std::vector<uint64_t> lens;
         std::vector<int8_t> labels;
         size_t err_line = SIZE_MAX;  // index into the round's lines
@@ -370,9 +375,11 @@ private:
                 if (s == e) continue;  // blank line: skipped, but numbered
                 int8_t label = 1;
                 const size_t before = fr.ids.size();
-                if (!parse_line(buf_.data() + s, line0 + i + 1, fr.ids, label, fr.err)) {
+                if (!parse_line(buf_.data() + s, line0 + i + 1, fr.ids, label, fr.err,
+                                binary_ ? nullptr : &fr.vals)) {
                     fr.err_line = i;
                     fr.ids.resize(before);
+                    if (!binary_) fr.vals.resize(before);
                     return;
                 }
                 fr.lens.push_back(fr.ids.size() - before);
@@ -393,6 +400,7 @@ private:
             const uint64_t base = b.nids();
             if (base + fr.ids.size() > b.cap_ids) b.reserve_ids(base + fr.ids.size() + (1u << 20));
             std::memcpy(b.ids + base, fr.ids.data(), fr.ids.size() * sizeof(uint32_t));
+            if (!binary_) b.vals.insert(b.vals.end(), fr.vals.begin(), fr.vals.end());
             uint64_t acc = base;
             for (size_t r = 0; r < fr.lens.size(); ++r) {
                 acc += fr.lens[r];
@@ -408,6 +416,7 @@ private:
 
     std::string path_;
     unsigned threads_;
+    bool binary_;
     FILE* f_ = nullptr;
     std::vector<char> buf_;
     size_t pos_ = 0, len_ = 0;
@@ -417,14 +426,67 @@ private:
 
 }  // namespace
 
-std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned parse_threads) {
+SketchFileReader::SketchFileReader(const std::string& path) {
+    f_ = open_or_fail(path, "rb");
+    try {
+        uint8_t h[36];
+        read_exact(f_, h, 4);
+        if (std::memcmp(h, "BBMH", 4) != 0)
+            fail(Errc::MalformedLine, path + ": not a BBMH sketch file");
+        read_exact(f_, h + 4, 4);
+        if (h[4] != 1) fail(Errc::MalformedLine, path + ": unknown version");
+        if (h[5] > 3) fail(Errc::MalformedLine, path + ": unknown scheme tag");
+        read_exact(f_, h + 8, 28);
+        scheme_ = h[5];
+        b_ = h[6];
+        k_ = get_u32(h + 8);
+        dim_ = get_u64(h + 12);
+        seed_ = get_u64(h + 20);
+        count_ = get_u64(h + 28);
+    } catch (...) {
+        std::fclose(f_);
+        f_ = nullptr;
+        throw;
+    }
+}
+
+SketchFileReader::~SketchFileReader() {
+    if (f_) std::fclose(f_);
+}
+
+uint64_t SketchFileReader::read(uint64_t max_rows, std::vector<uint8_t>& codes,
+                                std::vector<uint8_t>& flags, std::vector<int8_t>& labels) {
+    if (short_) fail(Errc::Io, "short read");
+    const uint64_t want = std::min(max_rows, count_ - done_);
+    if (want == 0) return 0;
+    const size_t cb = packed_code_bytes(k_, b_);
+    const size_t rec = 2 + cb;
+    buf_.resize(want * rec);
+    const size_t got = std::fread(buf_.data(), 1, want * rec, f_);
+    const uint64_t n = got / rec;
+    if (n < want) short_ = true;
+    if (n == 0) fail(Errc::Io, "short read");
+    codes.resize(n * cb);
+    flags.resize(n);
+    labels.resize(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        labels[i] = int8_t(buf_[i * rec]);
+        flags[i] = buf_[i * rec + 1];
+        std::memcpy(codes.data() + i * cb, buf_.data() + i * rec + 2, cb);
+    }
+    done_ += n;
+    return n;
+}
+
+std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned parse_threads,
+                                          bool libsvm_values) {
     FILE* f = open_or_fail(path, "rb");
     char magic[4] = {0, 0, 0, 0};
     const size_t got = std::fread(magic, 1, 4, f);
     std::fclose(f);
     if (got == 4 && std::memcmp(magic, "BBCV", 4) == 0)
         return std::make_unique<BinaryReader>(path, parse_threads);
-    return std::make_unique<LibsvmReader>(path, parse_threads);
+    return std::make_unique<LibsvmReader>(path, parse_threads, !libsvm_values);
 }
 
 }  // namespace bbmh

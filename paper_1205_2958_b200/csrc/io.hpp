@@ -27,12 +27,14 @@ struct Batch {
     std::vector<int8_t> labels;
     uint32_t* ids = nullptr;  // pinned
     uint64_t cap_ids = 0;
+    std::vector<float> vals;  // per-id values (LibSVM value mode only)
     ~Batch();
     void reserve_ids(uint64_t cap);  // keeps contents
     void clear() {
         n = 0;
         row_ptr.assign(1, 0);
         labels.clear();
+        vals.clear();
     }
     uint64_t nids() const { return row_ptr.back(); }
 };
@@ -47,7 +49,39 @@ public:
 };
 
 // open_corpus: sniff the "BBCV" magic, else LibSVM text (dataio.cpp:257-264).
-std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned parse_threads);
+// libsvm_values: keep real values instead of requiring 1 (the prediction
+// row source, learner.cpp:236-256).
+std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned parse_threads,
+                                          bool libsvm_values = false);
+
+// BBMH sketch file reader (SketchReader, sketch.cpp:143-207): header checks
+// with the reference's messages, then records in batches (label, flags,
+// ceil(k*b/8) code bytes each). A truncated record raises Io "short read"
+// after the complete records before it have been returned.
+class SketchFileReader {
+public:
+    explicit SketchFileReader(const std::string& path);
+    ~SketchFileReader();
+    SketchFileReader(const SketchFileReader&) = delete;
+    SketchFileReader& operator=(const SketchFileReader&) = delete;
+    uint32_t k() const { return k_; }
+    uint32_t b() const { return b_; }
+    uint8_t scheme() const { return scheme_; }
+    uint64_t dim() const { return dim_; }
+    uint64_t seed() const { return seed_; }
+    uint64_t count() const { return count_; }
+    // Up to max_rows records; returns how many (0 at the end).
+    uint64_t read(uint64_t max_rows, std::vector<uint8_t>& codes, std::vector<uint8_t>& flags,
+                  std::vector<int8_t>& labels);
+
+private:
+    FILE* f_ = nullptr;
+    uint32_t k_ = 0, b_ = 0;
+    uint8_t scheme_ = 0;
+    uint64_t dim_ = 0, seed_ = 0, count_ = 0, done_ = 0;
+    bool short_ = false;
+    std::vector<uint8_t> buf_;
+};
 
 // little-endian helpers
 inline void put_u32(uint8_t* p, uint32_t v) {

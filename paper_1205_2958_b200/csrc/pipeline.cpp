@@ -328,8 +328,6 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
     return stats;
 }
 
-namespace {
-
 // load_model (learner.cpp:588-612): "BBLM", u64 dim, u8 loss, u8 averaging,
 // dim doubles w, [dim doubles w_avg]; decision weights = averaging ? w_avg : w
 std::vector<double> load_decision_weights(const std::string& path) {
@@ -355,8 +353,6 @@ std::vector<double> load_decision_weights(const std::string& path) {
     if (tags[1]) read_exact(w.data(), dim * sizeof(double));  // w_avg replaces w
     return w;
 }
-
-}  // namespace
 
 PipelineStats predict_file(const Family& f, uint8_t b, const std::string& model_path,
                            const std::string& corpus_path, const std::string& scores_path,

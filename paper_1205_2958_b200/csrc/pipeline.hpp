@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "core.hpp"
 
@@ -30,6 +31,15 @@ PipelineStats sketch_file(const Family& f, const std::string& input_path,
 PipelineStats predict_file(const Family& f, uint8_t b, const std::string& model_path,
                            const std::string& corpus_path, const std::string& scores_path,
                            uint32_t workers, double* accuracy);
+
+// load_model (learner.cpp:588-612) -> decision weights (w_avg when averaged).
+std::vector<double> load_decision_weights(const std::string& path);
+
+// bbmh_predict (capi.cpp:307-317) on the GPU: BBMH / BBCV / LibSVM rows scored
+// against a BBLM model; writes the "%d\t%.9g" table (path "" = none, "-" =
+// stdout) and returns the accuracy.
+double predict_data(const std::string& model_path, const char* data_path,
+                    const std::string& scores_path, unsigned threads);
 
 // expand_stream (expansion.cpp:47-90): BBMH sketch -> BBCV rows or LibSVM text.
 uint64_t expand_file(const std::string& sketch_path, const std::string& out_path, bool binary);
