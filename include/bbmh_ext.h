@@ -60,6 +60,21 @@ BBMH_API bbmh_status bbmh_ext_predict_corpus(const bbmh_family* family, uint32_t
                                              const char* scores_path, uint32_t workers,
                                              double* accuracy_out);
 
+/* All-pairs b-bit matching counts (near-duplicate detection): the count of
+ * estimate_bbit (proj/src/estimator.cpp:53-58) for every pair of two sketch
+ * sets, on the GPU. codes_a: na rows, codes_b: nb rows, ceil(k*b/8) bytes
+ * each (LE bitstream); counts_out[i*nb + j] = #{t < k : code_t(A_i) ==
+ * code_t(B_j)}. Feed counts/k to the Theorem-1 correction
+ * (bbmh_correction_terms) for resemblance estimates. */
+BBMH_API bbmh_status bbmh_ext_match_counts(const uint8_t* codes_a, uint64_t na,
+                                           const uint8_t* codes_b, uint64_t nb, uint32_t k,
+                                           uint32_t b, uint32_t* counts_out);
+/* Same on device buffers, enqueued on `stream` (cudaStream_t). */
+BBMH_API bbmh_status bbmh_ext_match_counts_device(const uint8_t* d_codes_a, uint64_t na,
+                                                  const uint8_t* d_codes_b, uint64_t nb,
+                                                  uint32_t k, uint32_t b, uint32_t* d_counts,
+                                                  void* stream);
+
 /* Device list used by bbmh_ext_sketch_csr and bbmh_sketch_file (default:
  * the current device only). Chunks are assigned dynamically; output order
  * and bytes do not depend on the device count. */

@@ -14,6 +14,7 @@
 #include "../../include/bbmh_ext.h"
 #include "core.hpp"
 #include "engine.hpp"
+#include "estimate.hpp"
 #include "pipeline.hpp"
 
 using namespace bbmh;
@@ -293,33 +294,112 @@ bbmh_status bbmh_ext_set_chunk_docs(uint64_t docs) {
     return guarded([&] { set_chunk_docs(docs); });
 }
 
-// ---- outside the preprocessing path (bbmh.h:102-211 of the reference) -------
-bbmh_status bbmh_correction_terms(uint64_t, uint64_t, uint64_t, uint64_t, uint32_t, double*,
-                                  double*) {
-    return not_provided("bbmh_correction_terms");
+// ---- resemblance estimation (capi.cpp:187-240) ---------------
+static void put_estimate(const Estimate& e, bbmh_estimate* out) {
+    *out = {e.r_hat, e.r_raw, e.p_hat, e.c1b, e.c2b, e.var_theory};
 }
-bbmh_status bbmh_theoretical_variance(uint64_t, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t,
-                                      double*) {
-    return not_provided("bbmh_theoretical_variance");
+
+bbmh_status bbmh_correction_terms(uint64_t f1, uint64_t f2, uint64_t a, uint64_t dim, uint32_t b,
+                                  double* c1b_out, double* c2b_out) {
+    return guarded([&] {
+        if (!c1b_out || !c2b_out) fail(Errc::InvalidArgument, "outputs must not be NULL");
+        const Correction c = correction_terms(Profile{f1, f2, a, dim}, b);
+        *c1b_out = c.c1b;
+        *c2b_out = c.c2b;
+    });
 }
-bbmh_status bbmh_estimate_codes(const uint8_t*, const uint8_t*, uint32_t, uint32_t, uint64_t,
-                                uint64_t, uint64_t, uint64_t, bbmh_estimate*) {
-    return not_provided("bbmh_estimate_codes");
+
+bbmh_status bbmh_theoretical_variance(uint64_t f1, uint64_t f2, uint64_t a, uint64_t dim,
+                                      uint32_t b, uint32_t k, double* out) {
+    return guarded([&] {
+        if (!out) fail(Errc::InvalidArgument, "out must not be NULL");
+        *out = theoretical_variance(Profile{f1, f2, a, dim}, b, k);
+    });
 }
-bbmh_status bbmh_estimate_minima(const uint64_t*, const uint64_t*, uint32_t, double*) {
-    return not_provided("bbmh_estimate_minima");
+
+bbmh_status bbmh_estimate_codes(const uint8_t* codes1, const uint8_t* codes2, uint32_t k,
+                                uint32_t b, uint64_t f1, uint64_t f2, uint64_t a, uint64_t dim,
+                                bbmh_estimate* out) {
+    return guarded([&] {
+        if (!codes1 || !codes2 || !out) fail(Errc::InvalidArgument, "codes and out required");
+        if (k < 1) fail(Errc::InvalidArgument, "k must be >= 1");
+        put_estimate(estimate_codes(codes1, codes2, k, b, Profile{f1, f2, a, dim}), out);
+    });
 }
-bbmh_status bbmh_estimate_file(const char*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t,
-                               int32_t, bbmh_estimate*, double*) {
-    return not_provided("bbmh_estimate_file");
+
+bbmh_status bbmh_estimate_minima(const uint64_t* minima1, const uint64_t* minima2, uint32_t k,
+                                 double* r_hat_out) {
+    return guarded([&] {
+        if (!minima1 || !minima2 || !r_hat_out)
+            fail(Errc::InvalidArgument, "minima and out required");
+        *r_hat_out = estimate_minima(minima1, minima2, k);
+    });
+}
+
+bbmh_status bbmh_estimate_file(const char* sketch_path, uint64_t record1, uint64_t record2,
+                               uint64_t f1, uint64_t f2, uint64_t a, int32_t use_minima,
+                               bbmh_estimate* out, double* r_full_out) {
+    return guarded([&] {
+        if (!out) fail(Errc::InvalidArgument, "out must not be NULL");
+        Estimate e;
+        // *out is filled before the full-minima step can fail (capi.cpp:235-239)
+        struct Fill {
+            Estimate* e;
+            bbmh_estimate* out;
+            bool armed = false;
+            ~Fill() {
+                if (armed) put_estimate(*e, out);
+            }
+        } fill{&e, out};
+        const std::string path = require(sketch_path, "sketch_path");
+        try {
+            estimate_file(path, record1, record2, f1, f2, a, use_minima || r_full_out, r_full_out,
+                          &e);
+        } catch (const Error& err) {
+            fill.armed = e.p_hat != 0 || e.c1b != 0;  // the b-bit part completed
+            throw;
+        }
+        put_estimate(e, out);
+    });
+}
+
+bbmh_status bbmh_ext_match_counts(const uint8_t* codes_a, uint64_t na, const uint8_t* codes_b,
+                                  uint64_t nb, uint32_t k, uint32_t b, uint32_t* counts_out) {
+    return guarded([&] {
+        if ((na && !codes_a) || (nb && !codes_b) || (na && nb && !counts_out))
+            fail(Errc::InvalidArgument, "codes and counts required");
+        if (k < 1) fail(Errc::InvalidArgument, "k must be >= 1");
+        if (b < 1 || b > 32) fail(Errc::InvalidArgument, "b must be in 1..32");
+        match_counts_host(codes_a, na, codes_b, nb, k, b, counts_out);
+    });
+}
+
+bbmh_status bbmh_ext_match_counts_device(const uint8_t* d_codes_a, uint64_t na,
+                                         const uint8_t* d_codes_b, uint64_t nb, uint32_t k,
+                                         uint32_t b, uint32_t* d_counts, void* stream) {
+    return guarded([&] {
+        if ((na && !d_codes_a) || (nb && !d_codes_b) || (na && nb && !d_counts))
+            fail(Errc::InvalidArgument, "codes and counts required");
+        if (k < 1) fail(Errc::InvalidArgument, "k must be >= 1");
+        if (b < 1 || b > 32) fail(Errc::InvalidArgument, "b must be in 1..32");
+        match_counts_device(d_codes_a, na, d_codes_b, nb, k, b, d_counts,
+                            static_cast<cudaStream_t>(stream));
+    });
 }
 bbmh_status bbmh_mse_experiment(int32_t, uint64_t, uint64_t, uint64_t, uint64_t, const uint32_t*,
                                 size_t, const uint32_t*, size_t, uint64_t, uint64_t, uint32_t,
                                 const char*) {
     return not_provided("bbmh_mse_experiment");
 }
-bbmh_status bbmh_vw_project_file(const char*, const char*, uint32_t, uint64_t) {
-    return not_provided("bbmh_vw_project_file");
+// capi.cpp:277-283 -> vw_project_file (vw.cpp:61-77), hashed/aggregated on the GPU
+bbmh_status bbmh_vw_project_file(const char* corpus_path, const char* out_path, uint32_t bins,
+                                 uint64_t seed) {
+    return guarded([&] {
+        // argument evaluation order of the reference build: out_path, then corpus_path
+        const char* out = require(out_path, "out_path");
+        const char* in = require(corpus_path, "corpus_path");
+        vw_project_file(in, out, bins, seed);
+    });
 }
 bbmh_status bbmh_train(const char*, const char*, const char*, const char*,
                        const bbmh_train_config*) {

@@ -454,6 +454,13 @@ SketchFileReader::~SketchFileReader() {
     if (f_) std::fclose(f_);
 }
 
+void SketchFileReader::seek(uint64_t i) {
+    const uint64_t rec = 2 + packed_code_bytes(k_, b_);
+    if (std::fseek(f_, long(36 + i * rec), SEEK_SET) != 0) fail(Errc::Io, "seek failed");
+    done_ = i;
+    short_ = false;
+}
+
 uint64_t SketchFileReader::read(uint64_t max_rows, std::vector<uint8_t>& codes,
                                 std::vector<uint8_t>& flags, std::vector<int8_t>& labels) {
     if (short_) fail(Errc::Io, "short read");

@@ -73,6 +73,8 @@ public:
     // Up to max_rows records; returns how many (0 at the end).
     uint64_t read(uint64_t max_rows, std::vector<uint8_t>& codes, std::vector<uint8_t>& flags,
                   std::vector<int8_t>& labels);
+    // Position at record i (SketchReader::record, sketch.cpp:190-201).
+    void seek(uint64_t i);
 
 private:
     FILE* f_ = nullptr;

@@ -41,6 +41,10 @@ std::vector<double> load_decision_weights(const std::string& path);
 double predict_data(const std::string& model_path, const char* data_path,
                     const std::string& scores_path, unsigned threads);
 
+// vw_project_file (vw.cpp:61-77): corpus -> signed random-bin LibSVM rows (GPU).
+uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_path,
+                         uint32_t bins, uint64_t seed);
+
 // expand_stream (expansion.cpp:47-90): BBMH sketch -> BBCV rows or LibSVM text.
 uint64_t expand_file(const std::string& sketch_path, const std::string& out_path, bool binary);
 
