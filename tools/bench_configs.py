@@ -202,6 +202,110 @@ def run_loader(tmp, n_docs):
               "parse_threads": threads})
 
 
+def run_next(tmp):
+    """SURVEY §8f rows on the config-1 corpus, GPU vs the reference on this host:
+    prediction on sketches (fused corpus->score and bbmh_predict on a BBMH file),
+    all-pairs matching counts, and VW projection."""
+    import ctypes as C
+    from oracle import oracle as O
+    if not O.ref_available():
+        emit({"config": "next", "skipped": "oracle/_ref not built"})
+        return
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["c1"]
+    R = O.ref()
+    L = R.lib
+    L.bbmh_synth_classification.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_double,
+                                            C.c_double, C.c_double, C.c_uint64, C.c_int32]
+    corpus = os.path.join(tmp, "c1.bbcv")
+    if not os.path.exists(corpus):
+        assert L.bbmh_synth_classification(corpus.encode(), *golden["synth"]) == 0
+    threads = os.cpu_count() or 1
+    k, b, dim = 200, 8, 1 << 24
+    # -- prediction: reference = sketch_file + bbmh_predict(BBMH); ours = fused, and bbmh_predict
+    st, h = R.family(1, dim, k, 42)
+    sk = os.path.join(tmp, "p.bbmh")
+    t = time.perf_counter()
+    assert R.sketch_file(h, corpus, sk, b, 500, threads, False)[0] == 0
+    ref_sketch_s = time.perf_counter() - t
+    rng = np.random.default_rng(0)
+    w = rng.standard_normal(k << b)
+    model = os.path.join(tmp, "m.bblm")
+    with open(model, "wb") as fh:
+        fh.write(b"BBLM" + (k << b).to_bytes(8, "little") + bytes([0, 0]) + w.astype("<f8").tobytes())
+    L.bbmh_predict.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]
+    acc = C.c_double()
+    t = time.perf_counter()
+    assert L.bbmh_predict(model.encode(), sk.encode(), os.path.join(tmp, "r.tsv").encode(), C.byref(acc)) == 0
+    ref_predict_s = time.perf_counter() - t
+    f = bbmh.Family(1, dim, k, 42)
+    f.predict_corpus(b, model, corpus, os.path.join(tmp, "g.tsv"), threads)  # warm
+    t = time.perf_counter()
+    gacc = f.predict_corpus(b, model, corpus, os.path.join(tmp, "g.tsv"), threads)
+    fused_s = time.perf_counter() - t
+    same = open(os.path.join(tmp, "g.tsv"), "rb").read() == open(os.path.join(tmp, "r.tsv"), "rb").read()
+    lib = bbmh.lib()
+    lib.bbmh_predict.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]
+    t = time.perf_counter()
+    assert lib.bbmh_predict(model.encode(), sk.encode(), os.path.join(tmp, "g2.tsv").encode(), C.byref(acc)) == 0
+    gpu_predict_s = time.perf_counter() - t
+    emit({"config": "next_predict", "docs": 20000, "k": k, "b": b,
+          "ref_sketch_plus_predict_s": ref_sketch_s + ref_predict_s, "ref_threads": threads,
+          "gpu_fused_corpus_to_scores_s": fused_s, "gpu_bbmh_predict_on_sketch_s": gpu_predict_s,
+          "ref_bbmh_predict_on_sketch_s": ref_predict_s, "speedup_end_to_end": (ref_sketch_s + ref_predict_s) / fused_s,
+          "tables_identical": same, "accuracy_equal": gacc == acc.value})
+    # -- all-pairs matching counts (near-duplicate detection), k=500, b=8
+    ka, bb8 = 500, 8
+    na = nb = 8192
+    A = rng.integers(0, 256, (na, ka), dtype=np.uint8)
+    B = A[rng.integers(0, na, nb)].copy()
+    B[rng.random(B.shape) < 0.5] = 7
+    counts = np.zeros(na * nb, np.uint32)
+    lib.bbmh_ext_match_counts.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64,
+                                          C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]
+    pa, pb = A.tobytes(), B.tobytes()
+    lib.bbmh_ext_match_counts(pa, na, pb, nb, ka, bb8, counts.ctypes.data_as(C.POINTER(C.c_uint32)))
+    t = time.perf_counter()
+    lib.bbmh_ext_match_counts(pa, na, pb, nb, ka, bb8, counts.ctypes.data_as(C.POINTER(C.c_uint32)))
+    gpu_pairs_s = time.perf_counter() - t
+    # device-only timing (codes resident)
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    dC = torch.empty(na * nb, dtype=torch.int32, device="cuda")
+    lib.bbmh_ext_match_counts_device.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                                 C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]
+    stm = torch.cuda.current_stream()
+    ms = dev_time(lambda: lib.bbmh_ext_match_counts_device(dA.data_ptr(), na, dB.data_ptr(), nb, ka,
+                                                           bb8, dC.data_ptr(), stm.cuda_stream), reps=3)
+    ns = 256  # reference on a row sample, all threads
+    rc = np.zeros(ns * nb, np.uint32)
+    Lb = C.CDLL(O.REFBENCH_SO)
+    Lb.refbench_estimate_pairs.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_char_p,
+                                           C.c_uint64, C.c_uint32, C.c_uint32,
+                                           C.POINTER(C.c_uint32), C.c_uint32]
+    Lb.refbench_estimate_pairs.restype = C.c_double
+    rs = Lb.refbench_estimate_pairs(O.REF_SO.encode(), A[:ns].tobytes(), ns, pb, nb, ka, bb8,
+                                    rc.ctypes.data_as(C.POINTER(C.c_uint32)), threads)
+    emit({"config": "next_match", "na": na, "nb": nb, "k": ka, "b": bb8,
+          "gpu_host_api_s": gpu_pairs_s, "gpu_kernel_ms": ms,
+          "gpu_pairs_per_s_kernel": na * nb / ms * 1e3,
+          "ref_pairs_per_s": ns * nb / rs, "ref_threads": threads,
+          "ref_sample_rows": ns, "counts_match_reference_sample": bool(np.array_equal(rc, counts[: ns * nb]))})
+    # -- VW projection, bins = 2^20
+    L.bbmh_vw_project_file.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64]
+    lib.bbmh_vw_project_file.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64]
+    t = time.perf_counter()
+    assert L.bbmh_vw_project_file(corpus.encode(), os.path.join(tmp, "vr.txt").encode(), 1 << 20, 3) == 0
+    ref_vw = time.perf_counter() - t
+    lib.bbmh_vw_project_file(corpus.encode(), os.path.join(tmp, "vg.txt").encode(), 1 << 20, 3)
+    t = time.perf_counter()
+    assert lib.bbmh_vw_project_file(corpus.encode(), os.path.join(tmp, "vg.txt").encode(), 1 << 20, 3) == 0
+    gpu_vw = time.perf_counter() - t
+    same = open(os.path.join(tmp, "vg.txt"), "rb").read() == open(os.path.join(tmp, "vr.txt"), "rb").read()
+    emit({"config": "next_vw", "docs": 20000, "bins": 1 << 20, "ref_s": ref_vw, "gpu_s": gpu_vw,
+          "speedup": ref_vw / gpu_vw, "output_identical": same,
+          "note": "reference vw_project_file is single-threaded (vw.cpp:61-77)"})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="pcie,c1,c5,loader,c4,c3")
@@ -227,6 +331,8 @@ def main():
                     run_c5()
                 elif what == "loader":
                     run_loader(tmp, args.loader_docs)
+                elif what == "next":
+                    run_next(tmp)
             except Exception as ex:  # keep going; record the failure
                 emit({"config": what, "error": repr(ex)})
             print(f"# {what} took {time.time() - t:.1f}s", file=sys.stderr, flush=True)
