@@ -58,7 +58,8 @@ BBMH_API bbmh_status bbmh_ext_sketch_score_csr(const bbmh_family* family, const 
 BBMH_API bbmh_status bbmh_ext_predict_corpus(const bbmh_family* family, uint32_t b,
                                              const char* model_path, const char* corpus_path,
                                              const char* scores_path, uint32_t workers,
-                                             double* accuracy_out);
+                                             double* accuracy_out,
+                                             bbmh_pipeline_stats* stats_out /* nullable */);
 
 /* All-pairs b-bit matching counts (near-duplicate detection): the count of
  * estimate_bbit (proj/src/estimator.cpp:53-58) for every pair of two sketch

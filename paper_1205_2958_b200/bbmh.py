@@ -90,7 +90,8 @@ def lib() -> C.CDLL:
                                        C.POINTER(C.c_double), C.c_uint64,
                                        C.POINTER(C.c_double)], C.c_int32),
         "bbmh_ext_predict_corpus": ([C.c_void_p, C.c_uint32, C.c_char_p, C.c_char_p, C.c_char_p,
-                                     C.c_uint32, C.POINTER(C.c_double)], C.c_int32),
+                                     C.c_uint32, C.POINTER(C.c_double),
+                                     C.POINTER(PipelineStats)], C.c_int32),
         "bbmh_ext_set_devices": ([i32p, C.c_uint32], C.c_int32),
         "bbmh_ext_get_devices": ([i32p, C.c_uint32, C.POINTER(C.c_uint32)], C.c_int32),
         "bbmh_ext_family_prepare": ([C.c_void_p, C.c_int32], C.c_int32),
@@ -224,13 +225,18 @@ class Family:
         return scores
 
     def predict_corpus(self, b: int, model_path, corpus_path, scores_path=None,
-                       workers: int = 1) -> float:
-        """bbmh_ext_predict_corpus: corpus + BBLM model -> scores table; returns accuracy."""
+                       workers: int = 1, stats: dict | None = None) -> float:
+        """bbmh_ext_predict_corpus: corpus + BBLM model -> scores table; returns accuracy
+        (pipeline stats are stored into `stats` when a dict is given)."""
         acc = C.c_double(0)
+        st = PipelineStats()
         _check(lib().bbmh_ext_predict_corpus(
             self.handle, b, None if model_path is None else os.fsencode(model_path),
             None if corpus_path is None else os.fsencode(corpus_path),
-            None if scores_path is None else os.fsencode(scores_path), workers, C.byref(acc)))
+            None if scores_path is None else os.fsencode(scores_path), workers, C.byref(acc),
+            C.byref(st)))
+        if stats is not None:
+            stats.update(st.as_dict())
         return acc.value
 
     def sketch_file(self, input_path, output_path, b: int, chunk_size: int = 10000,

@@ -239,14 +239,18 @@ bbmh_status bbmh_ext_sketch_score_csr(const bbmh_family* family, const uint64_t*
 
 bbmh_status bbmh_ext_predict_corpus(const bbmh_family* family, uint32_t b, const char* model_path,
                                     const char* corpus_path, const char* scores_path,
-                                    uint32_t workers, double* accuracy_out) {
+                                    uint32_t workers, double* accuracy_out,
+                                    bbmh_pipeline_stats* stats_out) {
     return guarded([&] {
         if (!family) fail(Errc::InvalidArgument, "family must not be NULL");
         const char* model = require(model_path, "model_path");
         const char* data = require(corpus_path, "corpus_path");
         if (workers < 1) fail(Errc::InvalidArgument, "workers must be >= 1");
-        predict_file(*family->impl, uint8_t(b), model, data, scores_path ? scores_path : "",
-                     workers, accuracy_out);
+        PipelineStats st = predict_file(*family->impl, uint8_t(b), model, data,
+                                        scores_path ? scores_path : "", workers, accuracy_out);
+        if (stats_out)
+            *stats_out = {st.records,         st.chunks,        st.read_seconds,
+                          st.compute_seconds, st.write_seconds, st.wall_seconds};
     });
 }
 

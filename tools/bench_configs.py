@@ -239,8 +239,9 @@ def run_next(tmp):
     ref_predict_s = time.perf_counter() - t
     f = bbmh.Family(1, dim, k, 42)
     f.predict_corpus(b, model, corpus, os.path.join(tmp, "g.tsv"), threads)  # warm
+    pstats = {}
     t = time.perf_counter()
-    gacc = f.predict_corpus(b, model, corpus, os.path.join(tmp, "g.tsv"), threads)
+    gacc = f.predict_corpus(b, model, corpus, os.path.join(tmp, "g.tsv"), threads, stats=pstats)
     fused_s = time.perf_counter() - t
     same = open(os.path.join(tmp, "g.tsv"), "rb").read() == open(os.path.join(tmp, "r.tsv"), "rb").read()
     lib = bbmh.lib()
@@ -252,7 +253,7 @@ def run_next(tmp):
           "ref_sketch_plus_predict_s": ref_sketch_s + ref_predict_s, "ref_threads": threads,
           "gpu_fused_corpus_to_scores_s": fused_s, "gpu_bbmh_predict_on_sketch_s": gpu_predict_s,
           "ref_bbmh_predict_on_sketch_s": ref_predict_s, "speedup_end_to_end": (ref_sketch_s + ref_predict_s) / fused_s,
-          "tables_identical": same, "accuracy_equal": gacc == acc.value})
+          "tables_identical": same, "accuracy_equal": gacc == acc.value, "fused_stats": pstats})
     # -- all-pairs matching counts (near-duplicate detection), k=500, b=8
     ka, bb8 = 500, 8
     na = nb = 8192
