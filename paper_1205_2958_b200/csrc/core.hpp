@@ -46,6 +46,10 @@ private:
 
 [[noreturn]] inline void fail(Errc code, std::string msg) { throw Error(code, std::move(msg)); }
 
+// Developer tracing: with BBMH_TRACE=1 in the environment, prints
+// "bbmh-trace <ms since first call> <what>" to stderr (pipeline stage timing).
+void trace(const char* what);
+
 // ---- counter-based PRNG (src/prng.hpp:10-61), bit-exact ------------------
 constexpr uint64_t mix64(uint64_t x) {
     x ^= x >> 30;

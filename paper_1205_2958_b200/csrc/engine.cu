@@ -244,18 +244,23 @@ void set_chunk_docs(uint64_t docs) {
 // ---- Lane ------------------------------------------------------------------
 Lane::Lane(const Family& f, int device, uint32_t b, bool want_minima, const ScoreModel* score)
     : f_(f), device_(device), b_(b), cb_(packed_code_bytes(f.k, b)), want_minima_(want_minima) {
+    trace("lane: ctor");
     df_ = &device_family(f, device);
+    trace("lane: family resident");
     for (int i = 0; i < kSlots; ++i) slots_[i] = acquire_slot(device);
+    trace("lane: slots acquired");
     if (score) {
         DeviceGuard g(device);
         wdim_ = score->dim;
         BBMH_CUDA(cudaMalloc(&d_w_, std::max<uint64_t>(wdim_, 1) * sizeof(double)));
         if (wdim_)
             BBMH_CUDA(cudaMemcpy(d_w_, score->w, wdim_ * sizeof(double), cudaMemcpyHostToDevice));
+        trace("lane: model uploaded");
     }
 }
 
 Lane::~Lane() {
+    trace("lane: dtor");
     for (int i = 0; i < kSlots; ++i) {
         if (slots_[i] && slots_[i]->busy) cudaStreamSynchronize(slots_[i]->st);
         release_slot(slots_[i]);
@@ -267,6 +272,7 @@ Lane::~Lane() {
         cudaFree(d_w_);
         cudaSetDevice(prev);
     }
+    trace("lane: dtor done");
 }
 
 void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) {
@@ -315,6 +321,7 @@ void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) 
 }
 
 void Lane::enqueue(Slot& s, const ChunkJob& job) {
+    trace("lane: enqueue");
     const uint64_t n = job.n;
     const uint64_t nidx = job.row_ptr[n] - job.index_base;
     const bool stage = !job.pinned_input;
@@ -361,6 +368,7 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
 
 ChunkResult Lane::finish(Slot& s) {
     BBMH_CUDA(cudaEventSynchronize(s.done));
+    trace("lane: chunk done");
     s.busy = false;
     if (*s.h_err & 1)
         fail(Errc::InvalidArgument, "feature id out of range for the permutation universe");

@@ -11,11 +11,26 @@
 #include <algorithm>
 #include <atomic>
 #include <bit>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <thread>
 
 #include "core.hpp"
 
 namespace bbmh {
+
+void trace(const char* what) {
+    static const bool on = [] {
+        const char* e = std::getenv("BBMH_TRACE");
+        return e && *e && *e != '0';
+    }();
+    if (!on) return;
+    static const auto t0 = std::chrono::steady_clock::now();
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "bbmh-trace %10.3f %s\n", ms, what);
+}
 
 bool is_prime_u64(uint64_t n) {  // hash_family.cpp:28-37
     if (n < 2) return false;

@@ -194,6 +194,7 @@ private:
 template <typename Append>
 PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool emit_minima,
                          const ScoreModel* score, Append&& append) {
+    trace("stream: start");
     PipelineStats stats;
     const size_t cb = packed_code_bytes(f.k, b);
     const std::vector<int> devs = pipeline_devices();
@@ -202,6 +203,7 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
 
     const size_t nbatches = 3 * devs.size() + 3;
     BatchLease storage(nbatches);  // pinned batches reused across calls
+    trace("stream: batches leased");
     BlockingQueue<Batch*> free_q, in_q;
     for (Batch* bt : storage.batches) free_q.push(bt);
     Reorder done;
@@ -229,6 +231,7 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
                 bt->reserve_ids(kBatchIds + kBatchIds / 4);
                 const bool got = reader.fill(*bt, max_docs, kBatchIds);
                 read_s += since(t0);
+                trace("reader: batch filled");
                 if (!got) break;
                 if (!b_ok) fail(Errc::InvalidArgument, "b must be in 1..32");  // sketch.cpp:73
                 bt->seq = seq++;
@@ -302,8 +305,10 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
     } catch (...) {
         record_error(std::current_exception());
     }
+    trace("stream: writer done");
     rd.join();
     for (auto& t : lanes) t.join();
+    trace("stream: joined");
     if (error) std::rethrow_exception(error);
     for (double ms : kernel_ms) stats.compute_seconds += ms * 1e-3;
     return stats;
@@ -358,9 +363,12 @@ PipelineStats predict_file(const Family& f, uint8_t b, const std::string& model_
                            const std::string& corpus_path, const std::string& scores_path,
                            uint32_t workers, double* accuracy) {
     const auto wall0 = Clock::now();
+    trace("predict: start");
     // bbmh_predict order (capi.cpp:307-317): model, data, then the scores table
     std::vector<double> w = load_decision_weights(model_path);
+    trace("predict: model loaded");
     auto reader = open_corpus(corpus_path, workers ? workers : 1);
+    trace("predict: corpus open");
     FILE* out = nullptr;
     if (!scores_path.empty()) {
         out = scores_path == "-" ? stdout : std::fopen(scores_path.c_str(), "wb");
@@ -385,6 +393,7 @@ PipelineStats predict_file(const Family& f, uint8_t b, const std::string& model_
         }
         n += ob.n;
     });
+    trace("predict: stream done");
     if (accuracy) *accuracy = n ? double(correct) / double(n) : 0.0;
     stats.wall_seconds = since(wall0);
     return stats;
