@@ -30,6 +30,8 @@ enum Op : int {
     OP_MIX_4U = 11,    // the 4U-bit fold step: IMAD.WIDE(+pair) + LEA.HI + VIADDMNMX
     OP_MIX_2U_REUSE = 12,  // 2 IMAD : 1 VIMNMX3 with the coefficients in fixed operand slots
     OP_MIX_2U_CONST = 13,  // 2 IMAD : 1 VIMNMX3 with the multiplier from the constant bank
+    OP_IMAD_IMM = 14,      // IMAD R, R, imm32, R (immediate multiplier)
+    OP_MIX_2U_IMM = 15,    // 2 IMAD(imm) : 1 VIMNMX3
 };
 
 template <int OP>
@@ -90,6 +92,15 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
                 const uint64_t v = (uint64_t)a[i] * c1 + c2;
                 const uint32_t s = (uint32_t)(v >> 32) + ((uint32_t)v >> 1);
                 a[i] = min(s, s + 0x80000001u);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_IMAD_IMM) {
+                asm volatile("mad.lo.u32 %0, %0, 0x9e3779b1, %1;" : "+r"(a[i]) : "r"(c2));
+            } else if constexpr (OP == OP_MIX_2U_IMM) {
+                uint32_t h0, h1;
+                asm volatile("mad.lo.u32 %0, %1, 0x9e3779b1, %2;" : "=r"(h0) : "r"(a[i]), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, 0x85ebca6b, %2;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(c1));
+                w[i] = h0;
+                a[i] = min(min(a[i], h0), h1);
                 asm volatile("" : "+r"(a[i]));
             } else if constexpr (OP == OP_MIX_2U_CONST) {
                 // multiplier straight from the kernel-parameter constant bank
@@ -159,6 +170,7 @@ __attribute__((visibility("default"))) double bbmh_intpeak_ops_per_thread(int op
         case OP_MIX_4U: return base * 3;     // IMAD.WIDE + LEA.HI + VIADDMNMX
         case OP_MIX_2U_REUSE: return base * 3;
         case OP_MIX_2U_CONST: return base * 3;
+        case OP_MIX_2U_IMM: return base * 3;
         default: return base;
     }
 }
@@ -191,6 +203,8 @@ __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, 
         case OP_MIX_4U: ms = run<OP_MIX_4U>(blocks, threads, sink, cyc, clk, st); break;
         case OP_MIX_2U_REUSE: ms = run<OP_MIX_2U_REUSE>(blocks, threads, sink, cyc, clk, st); break;
         case OP_MIX_2U_CONST: ms = run<OP_MIX_2U_CONST>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_IMAD_IMM: ms = run<OP_IMAD_IMM>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_2U_IMM: ms = run<OP_MIX_2U_IMM>(blocks, threads, sink, cyc, clk, st); break;
         default: return -2;
     }
     unsigned long long* h = new unsigned long long[blocks];
