@@ -320,14 +320,76 @@ void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) 
     }
 }
 
+namespace {
+constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+// Page-locked caller ids larger than this are DMA'd in place rather than
+// copied into the packed block.
+constexpr uint64_t kPackedPinnedIdsBytes = 1ull << 20;
+}  // namespace
+
+// Small or pageable chunks: everything the chunk moves goes through one
+// pinned block per slot, so a chunk costs one H2D, the kernel(s) and one D2H
+// (the online small-batch case is bound by these API calls, not by bytes).
+//   H2D  [0, off_err+16):        row_ptr | ids | err=0, bad=~0
+//   D2H  [off_err, blk_end):     err, bad | scores | flags | codes
+void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
+    const uint64_t n = job.n;
+    s.off_ids = align16((n + 1) * sizeof(uint64_t));
+    s.off_err = align16(s.off_ids + nidx * sizeof(uint32_t));
+    s.off_scores = s.off_err + 16;
+    s.off_flags = s.off_scores + (d_w_ ? n * sizeof(double) : 0);
+    s.off_codes = align16(s.off_flags + n);
+    s.blk_end = s.off_codes + n * cb_;
+    if (s.blk_end > s.cap_blk) {
+        const uint64_t cap = std::max<uint64_t>(s.blk_end, s.cap_blk + s.cap_blk / 2);
+        if (s.d_blk) BBMH_CUDA(cudaFree(s.d_blk));
+        if (s.h_blk) BBMH_CUDA(cudaFreeHost(s.h_blk));
+        s.d_blk = nullptr;
+        s.h_blk = nullptr;
+        BBMH_CUDA(cudaMalloc(&s.d_blk, cap));
+        BBMH_CUDA(cudaMallocHost(&s.h_blk, cap));
+        s.cap_blk = cap;
+    }
+    s.packed = true;
+    uint8_t* h = s.h_blk;
+    std::memcpy(h, job.row_ptr, (n + 1) * sizeof(uint64_t));
+    if (nidx) std::memcpy(h + s.off_ids, job.indices, nidx * sizeof(uint32_t));
+    std::memset(h + s.off_err, 0, 8);
+    std::memset(h + s.off_err + 8, 0xff, 8);
+    BBMH_CUDA(cudaMemcpyAsync(s.d_blk, h, s.off_err + 16, cudaMemcpyHostToDevice, s.st));
+    uint8_t* d = s.d_blk;
+    auto* d_err = reinterpret_cast<int*>(d + s.off_err);
+    auto* d_bad = reinterpret_cast<unsigned long long*>(d + s.off_err + 8);
+    if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
+    launch_sketch(df_->kf, reinterpret_cast<const uint64_t*>(d), job.index_base,
+                  reinterpret_cast<const uint32_t*>(d + s.off_ids), n, b_, d + s.off_codes,
+                  nullptr, d + s.off_flags, d_err, s.st);
+    BBMH_CUDA(cudaGetLastError());
+    if (d_w_) {
+        launch_score(d + s.off_codes, d + s.off_flags, n, f_.k, b_, d_w_, wdim_,
+                     reinterpret_cast<double*>(d + s.off_scores), d_bad, s.st);
+        BBMH_CUDA(cudaGetLastError());
+    }
+    if (timed_) BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
+    BBMH_CUDA(cudaMemcpyAsync(h + s.off_err, d + s.off_err, s.blk_end - s.off_err,
+                              cudaMemcpyDeviceToHost, s.st));
+    BBMH_CUDA(cudaEventRecord(s.done, s.st));
+    s.busy = true;
+}
+
 void Lane::enqueue(Slot& s, const ChunkJob& job) {
     trace("lane: enqueue");
     const uint64_t n = job.n;
     const uint64_t nidx = job.row_ptr[n] - job.index_base;
     const bool stage = !job.pinned_input;
     DeviceGuard g(device_);
-    reserve(s, n, nidx, stage);
     s.job = job;
+    if (!want_minima_ && (stage || nidx * sizeof(uint32_t) <= kPackedPinnedIdsBytes)) {
+        enqueue_packed(s, job, nidx);
+        return;
+    }
+    s.packed = false;
+    reserve(s, n, nidx, stage);
     // row_ptr always goes through the slot's pinned mirror (small)
     std::memcpy(s.h_rp, job.row_ptr, (n + 1) * sizeof(uint64_t));
     BBMH_CUDA(cudaMemcpyAsync(s.d_rp, s.h_rp, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
@@ -341,7 +403,7 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
         BBMH_CUDA(cudaMemcpyAsync(s.d_idx, src, nidx * sizeof(uint32_t), cudaMemcpyHostToDevice,
                                   s.st));
     BBMH_CUDA(cudaMemsetAsync(s.d_err, 0, sizeof(int), s.st));
-    BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
+    if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
     launch_sketch(df_->kf, s.d_rp, job.index_base, s.d_idx, n, b_, s.d_codes,
                   want_minima_ ? s.d_min : nullptr, s.d_flags, s.d_err, s.st);
     BBMH_CUDA(cudaGetLastError());
@@ -354,7 +416,7 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
         BBMH_CUDA(cudaMemcpyAsync(s.h_bad, s.d_bad, sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s.st));
     }
-    BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
+    if (timed_) BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
     if (n && cb_)
         BBMH_CUDA(cudaMemcpyAsync(s.h_codes, s.d_codes, n * cb_, cudaMemcpyDeviceToHost, s.st));
     if (want_minima_)
@@ -370,20 +432,34 @@ ChunkResult Lane::finish(Slot& s) {
     BBMH_CUDA(cudaEventSynchronize(s.done));
     trace("lane: chunk done");
     s.busy = false;
-    if (*s.h_err & 1)
-        fail(Errc::InvalidArgument, "feature id out of range for the permutation universe");
-    if (*s.h_err & 2) fail(Errc::InvalidArgument, "row_ptr must be non-decreasing");
+    int herr;
+    unsigned long long hbad = ~0ull;
     ChunkResult r;
     r.tag = s.job.tag;
     r.n = s.job.n;
-    r.codes = s.h_codes;
-    r.minima = want_minima_ ? s.h_min : nullptr;
-    r.flags = s.h_flags;
+    if (s.packed) {
+        std::memcpy(&herr, s.h_blk + s.off_err, sizeof(int));
+        std::memcpy(&hbad, s.h_blk + s.off_err + 8, sizeof(hbad));
+        r.codes = s.h_blk + s.off_codes;
+        r.minima = nullptr;
+        r.flags = s.h_blk + s.off_flags;
+        r.scores = d_w_ ? reinterpret_cast<const double*>(s.h_blk + s.off_scores) : nullptr;
+    } else {
+        herr = *s.h_err;
+        if (d_w_) hbad = *s.h_bad;
+        r.codes = s.h_codes;
+        r.minima = want_minima_ ? s.h_min : nullptr;
+        r.flags = s.h_flags;
+        r.scores = d_w_ ? s.h_scores : nullptr;
+    }
+    if (herr & 1)
+        fail(Errc::InvalidArgument, "feature id out of range for the permutation universe");
+    if (herr & 2) fail(Errc::InvalidArgument, "row_ptr must be non-decreasing");
     if (d_w_) {
-        if (*s.h_bad != ~0ull) {  // predict_score (learner.cpp:515-517), first offender in order
-            const uint64_t row = *s.h_bad >> 24;
-            const uint32_t j = uint32_t(*s.h_bad & 0xffffff);
-            const uint8_t* c = s.h_codes + row * cb_;
+        if (hbad != ~0ull) {  // predict_score (learner.cpp:515-517), first offender in order
+            const uint64_t row = hbad >> 24;
+            const uint32_t j = uint32_t(hbad & 0xffffff);
+            const uint8_t* c = r.codes + row * cb_;
             uint32_t code = 0;
             for (uint32_t i = 0; i < b_; ++i) {
                 const uint64_t pos = uint64_t(j) * b_ + i;
@@ -393,9 +469,8 @@ ChunkResult Lane::finish(Slot& s) {
             fail(Errc::DimensionExceeded,
                  "feature " + std::to_string(idx) + " >= dim " + std::to_string(wdim_));
         }
-        r.scores = s.h_scores;
     }
-    cudaEventElapsedTime(&r.kernel_ms, s.ev0, s.ev1);
+    if (timed_) cudaEventElapsedTime(&r.kernel_ms, s.ev0, s.ev1);
     return r;
 }
 
@@ -428,6 +503,7 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     auto run_device = [&](int dev) {
         try {
             Lane lane(f, dev, b, minima != nullptr, score);
+            lane.set_timed(false);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
                 if (codes) std::memcpy(codes + r0 * cb, res.codes, res.n * cb);

@@ -101,6 +101,8 @@ public:
         }
     }
     int device() const { return device_; }
+    // Record kernel start/stop events per chunk (ChunkResult::kernel_ms).
+    void set_timed(bool on) { timed_ = on; }
 
 public:
     struct Slot {
@@ -125,6 +127,13 @@ public:
         unsigned long long* h_bad = nullptr;
         uint64_t cap_scores = 0;
         uint64_t cap_rows = 0, cap_idx = 0, cap_idx_pinned = 0, cap_codes = 0, cap_min = 0;
+        // packed transfer block: one H2D [row_ptr | ids | err,bad] and one
+        // D2H [err,bad | scores | flags | codes] per chunk (see enqueue)
+        uint8_t* d_blk = nullptr;
+        uint8_t* h_blk = nullptr;
+        uint64_t cap_blk = 0;
+        bool packed = false;
+        size_t off_ids = 0, off_err = 0, off_scores = 0, off_flags = 0, off_codes = 0, blk_end = 0;
         bool busy = false;
         ChunkJob job;
     };
@@ -132,6 +141,7 @@ public:
 private:
     void reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx);
     void enqueue(Slot& s, const ChunkJob& job);
+    void enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx);
     ChunkResult finish(Slot& s);
 
     const Family& f_;
@@ -143,6 +153,7 @@ private:
     double* d_w_ = nullptr;  // device copy of the scoring model (owned by the lane)
     uint64_t wdim_ = 0;
     uint64_t next_ = 0;
+    bool timed_ = true;
     Slot* slots_[kSlots] = {};
 };
 

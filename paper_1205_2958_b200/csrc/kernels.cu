@@ -24,6 +24,9 @@
 //     memory, writing bytes coalesced.
 // Reference semantics: sketch.cpp:71-100, hash_family.hpp:24-63,77-109.
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 
@@ -384,12 +387,27 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     int tile = env_int("BBMH_TUNE_TILE", SCHEME == S_2U ? 1024 : (int)kDefaultTile);
     tile = tile < 64 ? 64 : tile > 16384 ? 16384 : tile & ~3;
     const size_t smem = (2 * (tile + 8) + sh.jtile) * sizeof(uint32_t);
-    int dev = 0, sms = 148, occ = 1;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.tpb, smem);
-    occ = occ < 1 ? 1 : occ;
+    // occupancy/attribute queries cost several microseconds each: do them once
+    // per (kernel instance, device, block shape, smem)
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, size_t>, std::pair<int, int>> cache;  // -> (sms, occ)
+    int sms = 148, occ = 1;
+    {
+        std::lock_guard lk(mu);
+        auto key = std::make_tuple(dev, sh.tpb, smem);
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.tpb, smem);
+            occ = occ < 1 ? 1 : occ;
+            it = cache.emplace(key, std::make_pair(sms, occ)).first;
+        }
+        sms = it->second.first;
+        occ = it->second.second;
+    }
     const int ctas_env = env_int("BBMH_TUNE_CTAS_PER_SM", 0);
     if (ctas_env > 0 && ctas_env < occ) occ = ctas_env;
     // persistent: one wave of CTAs per j-tile, each looping over documents
