@@ -55,6 +55,7 @@ uint64_t g_chunk_docs = 0;
 constexpr uint64_t kDefaultChunkDocs = 32768;
 constexpr uint64_t kChunkIdxCap = 1ull << 24;        // 16 Mi ids (64 MiB) per chunk
 constexpr uint64_t kChunkMinimaBytes = 256ull << 20;  // cap on a chunk's minima buffer
+constexpr uint64_t kMinSplitIds = 1ull << 20;         // smallest chunk a batch is split into
 
 std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
     auto df = std::make_unique<DeviceFamily>();
@@ -322,20 +323,19 @@ void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) 
 
 namespace {
 constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-// Page-locked caller ids larger than this are DMA'd in place rather than
-// copied into the packed block.
-constexpr uint64_t kPackedPinnedIdsBytes = 1ull << 20;
 }  // namespace
 
-// Small or pageable chunks: everything the chunk moves goes through one
-// pinned block per slot, so a chunk costs one H2D, the kernel(s) and one D2H
-// (the online small-batch case is bound by these API calls, not by bytes).
-//   H2D  [0, off_err+16):        row_ptr | ids | err=0, bad=~0
+// Chunks without minima: everything small the chunk moves goes through one
+// pinned block per slot, so a chunk costs one H2D (plus one for page-locked
+// caller ids, DMA'd in place), the kernel(s) and one D2H (the online
+// small-batch case is bound by these API calls, not by bytes).
+//   H2D  [0, off_err+16):        row_ptr | ids (pageable input only) | err=0, bad=~0
 //   D2H  [off_err, blk_end):     err, bad | scores | flags | codes
 void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     const uint64_t n = job.n;
+    const bool inline_ids = !job.pinned_input;
     s.off_ids = align16((n + 1) * sizeof(uint64_t));
-    s.off_err = align16(s.off_ids + nidx * sizeof(uint32_t));
+    s.off_err = align16(s.off_ids + (inline_ids ? nidx * sizeof(uint32_t) : 0));
     s.off_scores = s.off_err + 16;
     s.off_flags = s.off_scores + (d_w_ ? n * sizeof(double) : 0);
     s.off_codes = align16(s.off_flags + n);
@@ -353,16 +353,23 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     s.packed = true;
     uint8_t* h = s.h_blk;
     std::memcpy(h, job.row_ptr, (n + 1) * sizeof(uint64_t));
-    if (nidx) std::memcpy(h + s.off_ids, job.indices, nidx * sizeof(uint32_t));
+    if (inline_ids && nidx) std::memcpy(h + s.off_ids, job.indices, nidx * sizeof(uint32_t));
     std::memset(h + s.off_err, 0, 8);
     std::memset(h + s.off_err + 8, 0xff, 8);
-    BBMH_CUDA(cudaMemcpyAsync(s.d_blk, h, s.off_err + 16, cudaMemcpyHostToDevice, s.st));
     uint8_t* d = s.d_blk;
+    const uint32_t* d_ids = reinterpret_cast<const uint32_t*>(d + s.off_ids);
+    if (!inline_ids && nidx) {
+        grow_device(s.d_idx, s.cap_idx, std::max<uint64_t>(nidx, 4));
+        BBMH_CUDA(cudaMemcpyAsync(s.d_idx, job.indices, nidx * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, s.st));
+        d_ids = s.d_idx;
+    }
+    BBMH_CUDA(cudaMemcpyAsync(s.d_blk, h, s.off_err + 16, cudaMemcpyHostToDevice, s.st));
     auto* d_err = reinterpret_cast<int*>(d + s.off_err);
     auto* d_bad = reinterpret_cast<unsigned long long*>(d + s.off_err + 8);
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
-    launch_sketch(df_->kf, reinterpret_cast<const uint64_t*>(d), job.index_base,
-                  reinterpret_cast<const uint32_t*>(d + s.off_ids), n, b_, d + s.off_codes,
+    launch_sketch(df_->kf, reinterpret_cast<const uint64_t*>(d), job.index_base, d_ids, n, b_,
+                  d + s.off_codes,
                   nullptr, d + s.off_flags, d_err, s.st);
     BBMH_CUDA(cudaGetLastError());
     if (d_w_) {
@@ -384,7 +391,7 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
     const bool stage = !job.pinned_input;
     DeviceGuard g(device_);
     s.job = job;
-    if (!want_minima_ && (stage || nidx * sizeof(uint32_t) <= kPackedPinnedIdsBytes)) {
+    if (!want_minima_) {
         enqueue_packed(s, job, nidx);
         return;
     }
@@ -486,10 +493,16 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     // chunk boundaries: <= chunk_docs rows, <= kChunkIdxCap ids (unless one row is larger)
     uint64_t cap_docs = chunk_docs_setting();
     if (minima) cap_docs = std::max<uint64_t>(1, std::min<uint64_t>(cap_docs, kChunkMinimaBytes / (8ull * f.k)));
+    // A batch that is one chunk serialises H2D -> kernel -> D2H; splitting a
+    // mid-sized batch into ~4 chunks (>= kMinSplitIds ids each) lets the
+    // slots' streams overlap one chunk's copy with another's kernel.
+    const uint64_t total_ids = row_ptr[n] - row_ptr[0];
+    const uint64_t idx_cap =
+        std::min<uint64_t>(kChunkIdxCap, std::max<uint64_t>(kMinSplitIds, total_ids / 4));
     std::vector<uint64_t> bounds{0};
     for (uint64_t r = 0; r < n;) {
         uint64_t e = r + 1;
-        while (e < n && e - r < cap_docs && row_ptr[e + 1] - row_ptr[r] <= kChunkIdxCap) ++e;
+        while (e < n && e - r < cap_docs && row_ptr[e + 1] - row_ptr[r] <= idx_cap) ++e;
         bounds.push_back(e);
         r = e;
     }

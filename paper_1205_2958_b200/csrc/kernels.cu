@@ -41,6 +41,21 @@ constexpr uint32_t kP31 = 0x7fffffffu;
 
 std::atomic<uint64_t> g_launches{0};
 
+// SM count of the current device, cached (attribute queries cost microseconds)
+int device_sms() {
+    static std::atomic<int> cache[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    int v = cache[dev].load(std::memory_order_relaxed);
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
 enum : int { S_PERM = 0, S_2U = 1, S_4UMOD = 2, S_4UBIT = 3 };
 
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) {
@@ -400,7 +415,13 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
         auto it = cache.find(key);
         if (it == cache.end()) {
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            // the attribute is a per-function ceiling: set it to the device's
+            // opt-in maximum, not to this shape's smem, or a later launch of a
+            // larger shape of the same kernel would fail with invalid argument
+            int optin = 0;
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin > (int)smem ? optin : (int)smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.tpb, smem);
             occ = occ < 1 ? 1 : occ;
             it = cache.emplace(key, std::make_pair(sms, occ)).first;
@@ -415,8 +436,12 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     if (gx < 1) gx = 1;
     if (gx > n) gx = n;
     dim3 grid((unsigned)gx, sh.jtiles);
+    const cudaError_t pre = cudaPeekAtLastError();
     kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr, base, idx, n, b, sh.jtile, (uint32_t)tile, codes,
                                      minima, flags, err);
+    if (const cudaError_t e = cudaPeekAtLastError(); e != cudaSuccess)
+        fprintf(stderr, "bbmh: sketch launch failed (%s; before launch: %s) grid %u x %u tpb %d smem %zu\n",
+                cudaGetErrorString(e), cudaGetErrorString(pre), grid.x, grid.y, sh.tpb, smem);
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -436,12 +461,20 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
 
 }  // namespace
 
-LaunchShape choose_shape(uint32_t k, int scheme) {
-    // Cost = lane-slots (tiles * tpb * J, idle j >= k lanes included) scaled by
-    // the measured relative inefficiency of small J (one LDS.128 feeds 4*J
-    // evaluations; tools/tune.py, profiles/r02): 2U is issue-bound so J = 1
-    // costs ~30% and J = 8 is best; 4U is arithmetic-bound and flat in J.
-    // Ties prefer fewer CTAs per document.
+LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
+    // Each thread owns J hash functions and streams every staged id, so its
+    // serial work is ~J * eff per id, where eff is the measured relative
+    // inefficiency of small J (one LDS.128 feeds 4*J evaluations;
+    // tools/tune.py, profiles/r02): 2U is issue-bound so J = 1 costs ~35% and
+    // J = 8 is best; 4U is arithmetic-bound and flat in J. An SM saturates at
+    // about kSatThreads threads; below that, time is the per-thread serial
+    // work. Model: time ~ J * eff * max(1, threads / (sms * kSatThreads)),
+    // with threads = n * tiles * tpb. For large batches this is the lane-slot
+    // cost (idle j >= k lanes included); for small online batches it prefers
+    // more, thinner j-tiles so the batch still fills the GPU. Ties prefer
+    // fewer CTAs per document.
+    constexpr double kSatThreads = 384;
+    const double docs = n ? (double)n : 1e12;
     LaunchShape best;
     double best_cost = 1e300;
     const int Js[4] = {8, 4, 2, 1};
@@ -452,8 +485,10 @@ LaunchShape choose_shape(uint32_t k, int scheme) {
             const uint64_t jtile = (uint64_t)tpb * J;
             const uint64_t tiles = (k + jtile - 1) / jtile;
             if (tiles > 65535) continue;
-            const double cost = (double)(tiles * jtile) * eff * (1.0 + 0.01 * (double)tiles);
-            if (cost < best_cost) {
+            const double threads = docs * (double)tiles * tpb;
+            const double fill = threads / ((double)sms * kSatThreads);
+            const double cost = J * eff * (fill > 1.0 ? fill : 1.0) * (1.0 + 0.01 * (double)tiles);
+            if (cost < best_cost * (1.0 - 1e-9)) {
                 best_cost = cost;
                 best.J = J;
                 best.tpb = tpb;
@@ -477,7 +512,7 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
                    const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima,
                    uint8_t* flags, int* err, cudaStream_t st) {
     if (n == 0) return;
-    const LaunchShape sh = choose_shape(F.k, F.scheme);
+    const LaunchShape sh = choose_shape(F.k, F.scheme, n, device_sms());
     switch (F.scheme) {
         case S_2U:
             return dispatch_j<S_2U, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);

@@ -34,7 +34,9 @@ struct LaunchShape {
     uint32_t jtiles = 1;   // CTAs per document
 };
 
-LaunchShape choose_shape(uint32_t k, int scheme);
+// Block shape for k hash functions over n documents on a GPU with `sms` SMs
+// (n = 0: throughput shape for an unbounded batch).
+LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n = 0, int sms = 148);
 
 // Sketch rows [0, n) of a CSR block resident on the current device.
 // row_ptr values are offsets into `indices` after subtracting index_base.
