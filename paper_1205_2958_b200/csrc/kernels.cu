@@ -418,10 +418,14 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
             // the attribute is a per-function ceiling: set it to the device's
             // opt-in maximum, not to this shape's smem, or a later launch of a
             // larger shape of the same kernel would fail with invalid argument
+            // (opt-in block limit minus the kernel's static shared memory)
             int optin = 0;
             cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, kern);
+            const int dyn_max = optin - (int)fa.sharedSizeBytes;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 optin > (int)smem ? optin : (int)smem);
+                                 dyn_max > (int)smem ? dyn_max : (int)smem);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.tpb, smem);
             occ = occ < 1 ? 1 : occ;
             it = cache.emplace(key, std::make_pair(sms, occ)).first;
