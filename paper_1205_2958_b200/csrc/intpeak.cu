@@ -32,6 +32,12 @@ enum Op : int {
     OP_MIX_2U_CONST = 13,  // 2 IMAD : 1 VIMNMX3 with the multiplier from the constant bank
     OP_IMAD_IMM = 14,      // IMAD R, R, imm32, R (immediate multiplier)
     OP_MIX_2U_IMM = 15,    // 2 IMAD(imm) : 1 VIMNMX3
+    OP_MIX_2U_MIN2 = 16,   // 2 IMAD : 2 two-input VIMNMX (fewer ALU operands)
+    OP_MIX_1TO1 = 17,      // 1 IMAD : 1 VIMNMX3
+    OP_MIX_IADD_IMM = 18,  // 2 IMAD(imm) : 1 IADD3 with an immediate (1 register read)
+    OP_MIX_2U_G4 = 19,     // 4 IMAD sharing both coefficients : 2 VIMNMX3 (coefficient-major)
+    OP_MIX_2U_MOV = 20,    // 2 IMAD(imm) : 1 VIMNMX3, IMAD addend = fresh register
+    OP_MIX_2U_UR = 21,     // 2 IMAD(uniform-register multiplier) : 1 VIMNMX3
 };
 
 template <int OP>
@@ -39,6 +45,7 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
                                                      unsigned long long* cycles,
                                                      unsigned long long* clk) {
     uint32_t a[kIlp], c1 = seed * 3 + 1, c2 = seed ^ 0x9e3779b9u;
+    const uint32_t c1v = c1 + threadIdx.x * 0x10001u;  // per-lane (not uniform) addend
     uint64_t w[kIlp];
 #pragma unroll
     for (int i = 0; i < kIlp; ++i) {
@@ -99,6 +106,51 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
                 uint32_t h0, h1;
                 asm volatile("mad.lo.u32 %0, %1, 0x9e3779b1, %2;" : "=r"(h0) : "r"(a[i]), "r"(c2));
                 asm volatile("mad.lo.u32 %0, %1, 0x85ebca6b, %2;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(c1));
+                w[i] = h0;
+                a[i] = min(min(a[i], h0), h1);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_MIX_2U_MIN2) {
+                uint32_t h0, h1;
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h0) : "r"(a[i]), "r"(c1), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(c1), "r"(c2));
+                w[i] = h0;
+                asm volatile("min.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(h0));
+                asm volatile("min.u32 %0, %0, %1;" : "+r"(a[i]) : "r"(h1));
+            } else if constexpr (OP == OP_MIX_1TO1) {
+                uint32_t h0;
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h0) : "r"(a[i]), "r"(c1), "r"(c2));
+                a[i] = min(min(a[i], h0), (uint32_t)w[i]);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_MIX_IADD_IMM) {
+                uint32_t h0, h1;
+                asm volatile("mad.lo.u32 %0, %1, 0x9e3779b1, %2;" : "=r"(h0) : "r"(a[i]), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, 0x85ebca6b, %2;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(c1));
+                w[i] = h0;
+                asm volatile("add.u32 %0, %1, 0x1234567;" : "=r"(a[i]) : "r"(h1));
+            } else if constexpr (OP == OP_MIX_2U_G4) {
+                // 4 ids t0..t3 (a[i], w lo/hi, a[i^1]) through one coefficient pair
+                uint32_t h0, h1, h2, h3;
+                const uint32_t t2 = (uint32_t)(w[i] >> 32), t3 = a[i ^ 1];
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h0) : "r"(a[i]), "r"(c1), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(c1), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h2) : "r"(t2), "r"(c1), "r"(c2));
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h3) : "r"(t3), "r"(c1), "r"(c2));
+                w[i] = ((uint64_t)h2 << 32) | h0;
+                a[i] = min(min(a[i], h0), h1);
+                a[i] = min(min(a[i], h2), h3);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_MIX_2U_MOV) {
+                uint32_t h0, h1;
+                asm volatile("mad.lo.u32 %0, %1, 0x9e3779b1, %2;" : "=r"(h0) : "r"(a[i]), "r"((uint32_t)(w[i] >> 32)));
+                asm volatile("mad.lo.u32 %0, %1, 0x85ebca6b, %2;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(a[i ^ 1]));
+                w[i] = ((uint64_t)h1 << 32) | h0;
+                a[i] = min(min(a[i], h0), h1);
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_MIX_2U_UR) {
+                // multiplier warp-uniform (kernel parameter -> uniform register), addend per lane
+                uint32_t h0, h1;
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h0) : "r"(a[i]), "r"(c2), "r"(c1v));
+                asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h1) : "r"((uint32_t)w[i]), "r"(c2), "r"(c1v));
                 w[i] = h0;
                 a[i] = min(min(a[i], h0), h1);
                 asm volatile("" : "+r"(a[i]));
@@ -171,6 +223,12 @@ __attribute__((visibility("default"))) double bbmh_intpeak_ops_per_thread(int op
         case OP_MIX_2U_REUSE: return base * 3;
         case OP_MIX_2U_CONST: return base * 3;
         case OP_MIX_2U_IMM: return base * 3;
+        case OP_MIX_2U_MIN2: return base * 4;
+        case OP_MIX_1TO1: return base * 2;
+        case OP_MIX_IADD_IMM: return base * 3;
+        case OP_MIX_2U_G4: return base * 6;
+        case OP_MIX_2U_MOV: return base * 3;
+        case OP_MIX_2U_UR: return base * 3;
         default: return base;
     }
 }
@@ -205,6 +263,12 @@ __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, 
         case OP_MIX_2U_CONST: ms = run<OP_MIX_2U_CONST>(blocks, threads, sink, cyc, clk, st); break;
         case OP_IMAD_IMM: ms = run<OP_IMAD_IMM>(blocks, threads, sink, cyc, clk, st); break;
         case OP_MIX_2U_IMM: ms = run<OP_MIX_2U_IMM>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_2U_MIN2: ms = run<OP_MIX_2U_MIN2>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_1TO1: ms = run<OP_MIX_1TO1>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_IADD_IMM: ms = run<OP_MIX_IADD_IMM>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_2U_G4: ms = run<OP_MIX_2U_G4>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_2U_MOV: ms = run<OP_MIX_2U_MOV>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_2U_UR: ms = run<OP_MIX_2U_UR>(blocks, threads, sink, cyc, clk, st); break;
         default: return -2;
     }
     unsigned long long* h = new unsigned long long[blocks];

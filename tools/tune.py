@@ -29,11 +29,18 @@ def main():
     for scheme in schemes:
         sid, dim = bench.SCHEMES[scheme]
         fam = bbmh.Family(sid, dim, bench.K, bench.SEED)
+        for k_ in ("J", "TPB", "TILE", "CTAS_PER_SM", "G"):
+            os.environ.pop("BBMH_TUNE_" + k_, None)
+        fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, bench.B,
+                              d_codes.data_ptr(), stream=st.cuda_stream)
+        torch.cuda.synchronize()
+        ref_codes = d_codes.clone()
         for g in grid:
             os.environ["BBMH_TUNE_J"] = str(g["J"])
             os.environ["BBMH_TUNE_TPB"] = str(g["TPB"])
             os.environ["BBMH_TUNE_TILE"] = str(g["TILE"])
             os.environ["BBMH_TUNE_CTAS_PER_SM"] = str(g.get("CTAS", 0))
+            os.environ["BBMH_TUNE_G"] = str(g.get("G", 4))
 
             def step():
                 fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, bench.B,
@@ -49,9 +56,11 @@ def main():
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / reps
+            same = bool(torch.equal(d_codes, ref_codes))
+            d_codes.zero_()
             evals = n * bench.NNZ * bench.K
             print(json.dumps({"scheme": scheme, **g, "ms": round(ms, 3),
-                              "tevals": round(evals / ms / 1e9, 3)}), flush=True)
+                              "tevals": round(evals / ms / 1e9, 3), "codes_match_default": same}), flush=True)
 
 
 if __name__ == "__main__":
