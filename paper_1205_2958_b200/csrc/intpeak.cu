@@ -38,7 +38,14 @@ enum Op : int {
     OP_MIX_2U_G4 = 19,     // 4 IMAD sharing both coefficients : 2 VIMNMX3 (coefficient-major)
     OP_MIX_2U_MOV = 20,    // 2 IMAD(imm) : 1 VIMNMX3, IMAD addend = fresh register
     OP_MIX_2U_UR = 21,     // 2 IMAD(uniform-register multiplier) : 1 VIMNMX3
+    OP_DFMA = 22,          // DFMA (fp64 pipe)
+    OP_MIX_DFMA_IMAD = 23, // 1 DFMA : 1 IMAD (separate pipes?)
+    OP_EVAL_4U_HORNER = 24,  // one full 4U-bit evaluation as shipped (Horner, %D by IMAD.HI)
+    OP_EVAL_4U_POWERS = 25,  // 4U-bit from precomputed powers, one 64-bit reduction, %D in fp32
 };
+
+constexpr uint32_t kP = 0x7fffffffu;
+constexpr uint32_t kD = 16609143u;
 
 template <int OP>
 __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* sink,
@@ -47,10 +54,13 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
     uint32_t a[kIlp], c1 = seed * 3 + 1, c2 = seed ^ 0x9e3779b9u;
     const uint32_t c1v = c1 + threadIdx.x * 0x10001u;  // per-lane (not uniform) addend
     uint64_t w[kIlp];
+    double dv[kIlp];
+    const double dc1 = 1.0000001 + seed * 1e-9, dc2 = 0.5;
 #pragma unroll
     for (int i = 0; i < kIlp; ++i) {
         a[i] = threadIdx.x * 7 + i + seed;
         w[i] = a[i];
+        dv[i] = a[i] * 1e-3;
     }
     __syncthreads();
     unsigned long long g0 = 0, g1 = 0;
@@ -154,6 +164,52 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
                 w[i] = h0;
                 a[i] = min(min(a[i], h0), h1);
                 asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_DFMA) {
+                asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(dv[i]) : "d"(dc1), "d"(dc2));
+            } else if constexpr (OP == OP_MIX_DFMA_IMAD) {
+                asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(dv[i]) : "d"(dc1), "d"(dc2));
+                asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(c1), "r"(c2));
+            } else if constexpr (OP == OP_EVAL_4U_HORNER) {
+                // t2 = 2t (< 2^32), coefficients a3, 2a2, 2a1, 2a0 (c1, c2, c1^5, c2^7 stand-ins)
+                const uint32_t t2 = (a[i] & kP) << 1;
+                auto fold = [](uint32_t h, uint32_t t, uint32_t c) {
+                    const uint64_t v = (uint64_t)h * t + c;
+                    return (uint32_t)(v >> 32) + ((uint32_t)v >> 1);
+                };
+                uint32_t x = fold(c1 & kP, t2, c2 & ~1u);
+                x = min(x, x - kP);
+                x = fold(x, t2, (c1 ^ 5) & ~1u);
+                x = min(x, x - kP);
+                x = fold(x, t2, (c2 ^ 7) & ~1u);
+                x = min(min(x, x - kP), x - 2 * kP);
+                const uint32_t q = __umulhi(x, 0x8150ee2bu) >> 23;
+                x = x + q * (0u - kD);
+                w[i] = min((uint32_t)w[i], x);
+                a[i] += x;
+                asm volatile("" : "+r"(a[i]));
+            } else if constexpr (OP == OP_EVAL_4U_POWERS) {
+                // T1..T3 < p precomputed per id (here derived cheaply from the chain value)
+                const uint32_t T1 = a[i] & kP, T2 = (a[i] * 3) & kP, T3 = (a[i] ^ 0x5555) & kP;
+                uint64_t x = (uint64_t)(c1 & kP) * T3 + (c2 & kP);
+                x += (uint64_t)((c1 ^ 5) & kP) * T2;
+                x += (uint64_t)((c2 ^ 7) & kP) * T1;  // < 3 p^2 + p
+                const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+                uint32_t h2 = min(hi, hi - kP);                 // hi mod p (hi < 3*2^30)
+                uint32_t l2 = (lo >> 31) + (lo & kP);           // lo mod p, lazily (<= p)
+                uint32_t s = h2 + l2;                           // < 2^32
+                s = (s >> 31) + (s & kP);
+                s = s + h2;                                     // x = 2 hi + lo (mod p)
+                s = (s >> 31) + (s & kP);
+                s = min(s, s - kP);
+                // s % D in fp32: q in {floor(s/D) - 1, floor(s/D)}, then one correction
+                const float sf = __int_as_float(0x4B000000u + (s >> 8)) - 8388608.0f;
+                const float y = __fmaf_rn(sf, 256.0f / kD * (1.0f - 1.0f / 1048576.0f), 12582911.5f);
+                const int qq = __float_as_int(y) - 0x4B400000;
+                uint32_t r = s - (uint32_t)qq * kD;
+                r = min(r, r - kD);
+                w[i] = min((uint32_t)w[i], r);
+                a[i] += r;
+                asm volatile("" : "+r"(a[i]));
             } else if constexpr (OP == OP_MIX_2U_CONST) {
                 // multiplier straight from the kernel-parameter constant bank
                 uint32_t h0, h1;
@@ -183,7 +239,7 @@ __global__ void __launch_bounds__(256) intpeak_kernel(uint32_t seed, uint32_t* s
     }
     uint32_t acc = 0;
 #pragma unroll
-    for (int i = 0; i < kIlp; ++i) acc ^= a[i] ^ (uint32_t)w[i] ^ (uint32_t)(w[i] >> 32);
+    for (int i = 0; i < kIlp; ++i) acc ^= a[i] ^ (uint32_t)w[i] ^ (uint32_t)(w[i] >> 32) ^ (uint32_t)__double2uint_rz(dv[i]);
     if (acc == 0x12345678u) sink[0] = acc;
     if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
@@ -229,6 +285,9 @@ __attribute__((visibility("default"))) double bbmh_intpeak_ops_per_thread(int op
         case OP_MIX_2U_G4: return base * 6;
         case OP_MIX_2U_MOV: return base * 3;
         case OP_MIX_2U_UR: return base * 3;
+        case OP_MIX_DFMA_IMAD: return base * 2;
+        case OP_EVAL_4U_HORNER: return base;  // evaluations, not instructions
+        case OP_EVAL_4U_POWERS: return base;
         default: return base;
     }
 }
@@ -269,6 +328,10 @@ __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, 
         case OP_MIX_2U_G4: ms = run<OP_MIX_2U_G4>(blocks, threads, sink, cyc, clk, st); break;
         case OP_MIX_2U_MOV: ms = run<OP_MIX_2U_MOV>(blocks, threads, sink, cyc, clk, st); break;
         case OP_MIX_2U_UR: ms = run<OP_MIX_2U_UR>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_DFMA: ms = run<OP_DFMA>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_MIX_DFMA_IMAD: ms = run<OP_MIX_DFMA_IMAD>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_EVAL_4U_HORNER: ms = run<OP_EVAL_4U_HORNER>(blocks, threads, sink, cyc, clk, st); break;
+        case OP_EVAL_4U_POWERS: ms = run<OP_EVAL_4U_POWERS>(blocks, threads, sink, cyc, clk, st); break;
         default: return -2;
     }
     unsigned long long* h = new unsigned long long[blocks];

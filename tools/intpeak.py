@@ -18,7 +18,9 @@ OPS = {0: "imad", 1: "imad_wide+lea_hi", 2: "vimnmx3", 3: "iadd3", 4: "lop3",
        12: "mix_2u_reuse(2imad:1vimnmx3)", 13: "mix_2u_const(2imad:1vimnmx3)",
        14: "imad_imm", 15: "mix_2u_imm(2imad_imm:1vimnmx3)",
        16: "mix_2u_min2(2imad:2vimnmx)", 17: "mix_1to1(imad:vimnmx3)", 18: "mix_iadd_imm(2imad_imm:1iadd3)",
-       19: "mix_2u_g4(4imad:2vimnmx3)", 20: "mix_2u_mov(2imad_imm_fresh_c:1vimnmx3)"}
+       19: "mix_2u_g4(4imad:2vimnmx3)", 20: "mix_2u_mov(2imad_imm_fresh_c:1vimnmx3)",
+       21: "mix_2u_ur(2imad_ur:1vimnmx3)", 22: "dfma", 23: "mix_dfma_imad(1:1)",
+       24: "eval_4u_horner(evals)", 25: "eval_4u_powers_fp32modD(evals)"}
 SMS = 148
 
 

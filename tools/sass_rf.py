@@ -41,6 +41,8 @@ def parse(lines, a0, a1):
             r = re.match(r"-?\|?R(\d+)(\.reuse)?", o)
             if r:
                 regs.append((int(r.group(1)), slot, bool(r.group(2))))
+                if op.startswith("IMAD.WIDE") and slot == 2:  # 64-bit addend: register pair
+                    regs.append((int(r.group(1)) + 1, 10 + slot, bool(r.group(2))))
         out.append((op, regs))
     return out
 
