@@ -351,3 +351,54 @@ __attribute__((visibility("default"))) int bbmh_intpeak_run(int op, int blocks, 
     return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
 }
+
+// ---- L2 random-gather throughput (roofline denominator of permutation mode) ----
+namespace {
+__global__ void __launch_bounds__(256) l2gather_kernel(const uint32_t* __restrict__ tab, uint32_t mask,
+                                                       uint32_t iters, uint32_t seed, uint32_t* sink) {
+    uint32_t x = (blockIdx.x * blockDim.x + threadIdx.x) * 0x9e3779b9u ^ seed;
+    uint32_t m = 0xffffffffu;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    for (uint32_t it = 0; it < iters; ++it) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            x = x * 1664525u + 1013904223u;  // LCG: independent addresses, 8 loads in flight
+            asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;"
+                         : "=r"(v[u]) : "l"(tab + ((x >> 5) & mask)), "l"(pol));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m = min(m, v[u]);
+    }
+    if (m == 0x12345678u) sink[0] = m;
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int bbmh_l2gather_run(uint64_t table_bytes, int blocks,
+                                                                       int threads, uint32_t iters,
+                                                                       double* gathers_per_s) {
+    uint32_t* tab = nullptr;
+    uint32_t* sink = nullptr;
+    const uint64_t n = table_bytes / 4;
+    if ((n & (n - 1)) != 0) return -1;  // power of two entries
+    if (cudaMalloc(&tab, table_bytes) != cudaSuccess) return -2;
+    if (cudaMalloc(&sink, 4) != cudaSuccess) return -2;
+    cudaMemset(tab, 0x11, table_bytes);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    l2gather_kernel<<<blocks, threads>>>(tab, (uint32_t)(n - 1), iters, 1, sink);  // warm L2
+    cudaEventRecord(e0);
+    l2gather_kernel<<<blocks, threads>>>(tab, (uint32_t)(n - 1), iters, 2, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *gathers_per_s = (double)blocks * threads * iters * 8 / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(tab);
+    cudaFree(sink);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}

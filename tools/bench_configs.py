@@ -117,9 +117,18 @@ def run_c3(n_docs):
     ms = dev_time(lambda: f.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n_docs, 8,
                                               d_codes.data_ptr(), stream=st.cuda_stream), reps=2)
     evals = n_docs * bench.NNZ * k
+    # roofline: random 4-byte gathers from one L2-resident 64 MB table, all SMs
+    # (tools/intpeak.py l2_gathers), measured in this process
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import intpeak
+    l2 = intpeak.l2_gathers(sizes_mb=(64,))["64MB"] * 1e9
+    gps = evals / ms * 1e3
     emit({"config": "c3", "dim": dim, "k": k, "docs": n_docs, "table_bytes": dim * k * 4,
           "table_build_s": build_s, "upload_s": upload_s, "kernel_ms": ms,
-          "gathers_per_s": evals / ms * 1e3, "docs_per_s": n_docs / ms * 1e3,
+          "gathers_per_s": gps, "docs_per_s": n_docs / ms * 1e3,
+          "roofline": {"bound": "l2_random_gather", "achieved": gps, "peak": l2,
+                       "frac": gps / l2, "unit": "gathers/s",
+                       "peak_how": "intpeak.l2_gathers: 64 MB table, 8 CTAs x 256 threads per SM"},
           "sector_bound_gathers_per_s_at_hbm": 6461.2e9 / 32})
     f.close()
     del d_rp, d_idx, d_codes

@@ -49,9 +49,23 @@ def measure(blocks_per_sm=8, threads=256):
     return {"sms": SMS, "blocks_per_sm": blocks_per_sm, "threads": threads, "ops": res}
 
 
+def l2_gathers(sizes_mb=(16, 32, 64, 96, 1024), blocks_per_sm=8, threads=256, iters=256):
+    """Random 4-byte gathers per second from an L2-resident (or not) table of each size."""
+    L = C.CDLL(LIB)
+    L.bbmh_l2gather_run.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_uint32, C.POINTER(C.c_double)]
+    out = {}
+    for mb in sizes_mb:
+        g = C.c_double()
+        st = L.bbmh_l2gather_run(mb << 20, SMS * blocks_per_sm, threads, iters, C.byref(g))
+        out[f"{mb}MB"] = round(g.value / 1e9, 1) if st == 0 else {"error": st}
+    return {"unit": "G gathers/s", "blocks_per_sm": blocks_per_sm, "threads": threads, **out}
+
+
 if __name__ == "__main__":
     r = measure()
+    r["l2_gathers"] = l2_gathers()
     print(json.dumps(r, indent=1))
     if len(sys.argv) > 1:
         with open(sys.argv[1], "w") as f:
             json.dump(r, f, indent=1)
+
