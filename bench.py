@@ -154,7 +154,9 @@ def int_peaks():
     """Measured per-SM integer pipe rates (tools/intpeak.py)."""
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import intpeak
-    return intpeak.measure()
+    # only the rates the roofline formulas below use
+    return intpeak.measure(only={"imad", "vimnmx3", "imad_wide+lop3", "imad_hi",
+                                 "mix_2u_reuse(2imad:1vimnmx3)"})
 
 
 def pipe_costs(scheme, dim, peaks):

@@ -337,9 +337,20 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
                 __syncthreads();
             }
             const uint4* b4 = reinterpret_cast<const uint4*>(buf);
+            // 2U: software-pipelined, the next quad loads under this one's IMADs (the
+            // LDS latency was the top short-scoreboard stall); the 4U schemes have
+            // enough arithmetic per quad to hide it and run slower with it
+            constexpr bool kPrefetch = SCHEME == S_2U;
+            uint4 tn = kPrefetch ? b4[0] : make_uint4(0, 0, 0, 0);
 #pragma unroll(J >= 8 ? 2 : 4)
             for (uint32_t q = 0; q < n4; ++q) {
-                const uint4 t4 = b4[q];
+                uint4 t4;
+                if constexpr (kPrefetch) {
+                    t4 = tn;
+                    tn = b4[min(q + 1, n4 - 1)];
+                } else {
+                    t4 = b4[q];
+                }
 #pragma unroll
                 for (int r = 0; r < J; ++r) {
                     const uint32_t h0 = hash1<SCHEME, POW2>(F, c[r], t4.x);

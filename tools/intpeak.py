@@ -24,7 +24,8 @@ OPS = {0: "imad", 1: "imad_wide+lea_hi", 2: "vimnmx3", 3: "iadd3", 4: "lop3",
 SMS = 148
 
 
-def measure(blocks_per_sm=8, threads=256):
+def measure(blocks_per_sm=8, threads=256, only=None):
+    """Rates of the OPS microbenchmarks (all, or the names in `only`)."""
     L = C.CDLL(LIB)
     L.bbmh_intpeak_run.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -33,6 +34,8 @@ def measure(blocks_per_sm=8, threads=256):
     res = {}
     blocks = SMS * blocks_per_sm
     for op, name in OPS.items():
+        if only is not None and name not in only:
+            continue
         ms, cyc, mhz = C.c_float(), C.c_double(), C.c_double()
         st = L.bbmh_intpeak_run(op, blocks, threads, C.byref(ms), C.byref(cyc), C.byref(mhz))
         if st != 0:
