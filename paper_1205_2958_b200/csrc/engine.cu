@@ -338,7 +338,7 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     s.off_err = align16(s.off_ids + (inline_ids ? nidx * sizeof(uint32_t) : 0));
     s.off_scores = s.off_err + 16;
     s.off_flags = s.off_scores + (d_w_ ? n * sizeof(double) : 0);
-    s.off_codes = align16(s.off_flags + n);
+    s.off_codes = s.off_flags + n;  // no gap: every byte copied back is written by a kernel
     s.blk_end = s.off_codes + n * cb_;
     if (s.blk_end > s.cap_blk) {
         const uint64_t cap = std::max<uint64_t>(s.blk_end, s.cap_blk + s.cap_blk / 2);
@@ -353,6 +353,10 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     s.packed = true;
     uint8_t* h = s.h_blk;
     std::memcpy(h, job.row_ptr, (n + 1) * sizeof(uint64_t));
+    // zero the alignment gaps too: every byte of the H2D block is defined
+    std::memset(h + (n + 1) * sizeof(uint64_t), 0, s.off_ids - (n + 1) * sizeof(uint64_t));
+    const size_t ids_end = s.off_ids + (inline_ids ? nidx * sizeof(uint32_t) : 0);
+    std::memset(h + ids_end, 0, s.off_err - ids_end);
     if (inline_ids && nidx) std::memcpy(h + s.off_ids, job.indices, nidx * sizeof(uint32_t));
     std::memset(h + s.off_err, 0, 8);
     std::memset(h + s.off_err + 8, 0xff, 8);

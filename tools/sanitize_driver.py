@@ -1,0 +1,75 @@
+"""Tiny invocation of every CUDA kernel in libbbmh.so, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck): sketch (2U, 4U-bit with
+power-of-two and general D, 4U-mod, permutation in both schedules, k
+spanning several CTAs, rows longer than one shared-memory tile, empty rows),
+the file pipeline + expansion to BBCV and LibSVM text, fused scoring,
+predict on a BBMH file, all-pairs match counts and the VW projection.
+No torch; ctypes only. Usage: compute-sanitizer --tool memcheck python
+tools/sanitize_driver.py"""
+import ctypes as C
+import os
+import struct
+import sys
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from helpers import bbcv_bytes, random_csr  # noqa: E402
+from paper_1205_2958_b200 import bbmh  # noqa: E402
+
+
+def main():
+    rng = np.random.default_rng(1)
+    rp, idx = random_csr(rng, 12, 1 << 20, 0, 700, empty_every=5)
+    long_rp, long_idx = random_csr(rng, 2, 1 << 20, 9000, 9000)
+    for scheme, dim, prime, k in ((1, 1 << 20, 0, 70), (3, 1 << 20, 0, 40), (3, 1000003, 0, 33),
+                                  (2, 1 << 20, 16777259, 20), (1, 1 << 20, 0, 2100)):
+        with bbmh.Family(scheme, dim, k, 42, prime) as f:
+            f.sketch_csr(rp, idx, 8, want_minima=True)
+            f.sketch_csr(long_rp, long_idx, 5)
+            f.sketch_set(idx[: int(rp[1])], 3)
+            f.sketch_score_csr(rp, idx, 4, rng.standard_normal(k << 4))
+    os.environ["BBMH_PERM_TABLEWISE"] = "1"
+    with bbmh.Family(0, 1 << 12, 9, 42) as f:
+        f.sketch_csr(rp, idx % (1 << 12), 6, want_minima=True)
+    os.environ["BBMH_PERM_TABLEWISE"] = "0"
+    with bbmh.Family(0, 1 << 12, 9, 42) as f:
+        f.sketch_csr(rp, idx % (1 << 12), 6)
+    with tempfile.TemporaryDirectory() as td:
+        rows = [(1 if i % 2 else -1, idx[int(rp[i]):int(rp[i + 1])]) for i in range(12)]
+        corpus = os.path.join(td, "c.bbcv")
+        open(corpus, "wb").write(bbcv_bytes(1 << 20, rows))
+        sk = os.path.join(td, "c.bbmh")
+        with bbmh.Family(1, 1 << 20, 30, 42) as f:
+            f.sketch_file(corpus, sk, 4, 5, 2)
+        bbmh.expand_file(sk, os.path.join(td, "e.txt"), bbmh.ROWS_LIBSVM)
+        bbmh.expand_file(sk, os.path.join(td, "e.bbcv"), bbmh.ROWS_BINARY)
+        model = os.path.join(td, "m.bblm")
+        w = rng.standard_normal(30 << 4)
+        open(model, "wb").write(b"BBLM" + struct.pack("<Q", w.size) + bytes([1, 0]) +
+                                w.astype("<f8").tobytes())
+        lib = bbmh.lib()
+        lib.bbmh_predict.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(C.c_double)]
+        acc = C.c_double()
+        assert lib.bbmh_predict(model.encode(), sk.encode(), os.path.join(td, "s.tsv").encode(),
+                                C.byref(acc)) == 0, bbmh.last_error()
+        lib.bbmh_vw_project_file.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64]
+        assert lib.bbmh_vw_project_file(corpus.encode(), os.path.join(td, "v.txt").encode(),
+                                        1 << 10, 3) == 0, bbmh.last_error()
+    k, b = 100, 4
+    cb = (k * b + 7) // 8
+    A = rng.integers(0, 256, (37, cb), dtype=np.uint8)
+    out = np.zeros(37 * 21, np.uint32)
+    lib = bbmh.lib()
+    lib.bbmh_ext_match_counts.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p, C.c_uint64,
+                                          C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]
+    assert lib.bbmh_ext_match_counts(A.tobytes(), 37, A[:21].tobytes(), 21, k, b,
+                                     out.ctypes.data_as(C.POINTER(C.c_uint32))) == 0, bbmh.last_error()
+    print("sanitize driver ok,", bbmh.kernel_launches(), "kernel launches")
+
+
+if __name__ == "__main__":
+    main()
