@@ -9,6 +9,7 @@
 // sharding, no collective): output position depends only on the chunk index.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -485,6 +486,74 @@ ChunkResult Lane::finish(Slot& s) {
     return r;
 }
 
+// ---- small pinned batches: zero-copy --------------------------------------
+namespace {
+
+// Zero-copy pays where the fixed per-call costs (H2D/D2H API calls) dominate:
+// 2U batches up to ~500 webspam rows. Larger batches overlap chunk copies with
+// kernels and the output memcpy in the chunked path (tools/zerocopy_probe.py,
+// profiles/r10/zerocopy.jsonl); 4U is kernel-bound at every batch size.
+constexpr uint64_t kZeroCopyMaxIds = 2ull << 20;
+
+// Device address of page-locked host memory (UVA mapping), or null.
+const void* mapped_device_ptr(const void* p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+// The kernel reads the caller's page-locked ids straight over PCIe (the TMA
+// bulk copies take host addresses; repeated reads hit L2) and stores codes and
+// flags into the slot's mapped pinned block, so a call is one launch and one
+// synchronisation, with no H2D/D2H API calls and no staging copy of the ids.
+// For small online batches those fixed costs dominate (profiles/r10: 2U k=500,
+// batch 64: 79 -> 74 us; batch 256: 161 -> 131 us through the host API).
+bool sketch_rows_zero_copy(const Family& f, int dev, const uint64_t* row_ptr,
+                           const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
+                           uint8_t* flags) {
+    const void* d_ids = mapped_device_ptr(indices);
+    if (!d_ids) return false;
+    DeviceGuard g(dev);
+    const DeviceFamily& df = device_family(f, dev);
+    Lane::Slot* s = acquire_slot(dev);
+    struct Release {
+        Lane::Slot* s;
+        ~Release() { release_slot(s); }
+    } rel{s};
+    const size_t cb = packed_code_bytes(f.k, b);
+    const size_t off_flags = align16((n + 1) * sizeof(uint64_t));
+    const size_t off_codes = off_flags + n;
+    const size_t need = off_codes + n * cb;
+    if (need > s->cap_blk) {
+        const uint64_t cap = std::max<uint64_t>(need, s->cap_blk + s->cap_blk / 2);
+        if (s->d_blk) BBMH_CUDA(cudaFree(s->d_blk));
+        if (s->h_blk) BBMH_CUDA(cudaFreeHost(s->h_blk));
+        s->d_blk = nullptr;
+        s->h_blk = nullptr;
+        BBMH_CUDA(cudaMalloc(&s->d_blk, cap));
+        BBMH_CUDA(cudaMallocHost(&s->h_blk, cap));
+        s->cap_blk = cap;
+    }
+    uint8_t* h = s->h_blk;  // cudaMallocHost memory: the same address is valid on the device
+    std::memcpy(h, row_ptr, (n + 1) * sizeof(uint64_t));
+    // err: the kernel only flags permutation ids >= D (not this path) and a
+    // decreasing row_ptr (rejected on the host before we get here)
+    launch_sketch(df.kf, reinterpret_cast<const uint64_t*>(h), 0,
+                  static_cast<const uint32_t*>(d_ids), n, b, h + off_codes, nullptr,
+                  h + off_flags, s->d_err, s->st);
+    BBMH_CUDA(cudaGetLastError());
+    BBMH_CUDA(cudaStreamSynchronize(s->st));
+    if (codes) std::memcpy(codes, h + off_codes, n * cb);
+    if (flags) std::memcpy(flags, h + off_flags, n);
+    return true;
+}
+
+}  // namespace
+
 // ---- host-buffer CSR entry -------------------------------------------------
 void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* indices,
                       uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima, uint8_t* flags,
@@ -493,6 +562,16 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     check_row_ptr(row_ptr, n);
     const size_t cb = packed_code_bytes(f.k, b);
     const bool pinned = is_pinned(indices);
+    static const bool zero_copy_on = [] {
+        const char* e = std::getenv("BBMH_ZERO_COPY");  // developer knob (A/B timing)
+        return !(e && *e == '0');
+    }();
+    if (zero_copy_on && pinned && !minima && !score && f.scheme == Scheme::TwoU &&
+        row_ptr[n] - row_ptr[0] <= kZeroCopyMaxIds) {
+        const std::vector<int> devs = pipeline_devices();
+        if (devs.size() == 1 && sketch_rows_zero_copy(f, devs[0], row_ptr, indices, n, b, codes, flags))
+            return;
+    }
 
     // chunk boundaries: <= chunk_docs rows, <= kChunkIdxCap ids (unless one row is larger)
     uint64_t cap_docs = chunk_docs_setting();
