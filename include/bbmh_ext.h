@@ -30,7 +30,13 @@ BBMH_API bbmh_status bbmh_ext_sketch_csr(const bbmh_family* family, const uint64
 /* Device buffers on the CURRENT device; enqueued on `stream` (a
  * cudaStream_t, NULL = legacy default stream) and returns without
  * synchronising. row_ptr values are offsets into d_indices after subtracting
- * `index_base` (lets a caller pass a slice of a larger row_ptr). */
+ * `index_base` (lets a caller pass a slice of a larger row_ptr).
+ * Ids are fetched with bulk copies in whole 16-byte granules, so the granule
+ * holding the last id (d_indices + row_ptr[n] - index_base) is read to its
+ * end: up to 12 bytes past the last id, never across a page. An allocation
+ * whose size is a multiple of 16 bytes (or with 12 bytes of slack) keeps
+ * compute-sanitizer memcheck quiet. The host entry points handle this
+ * themselves. */
 BBMH_API bbmh_status bbmh_ext_sketch_csr_device(const bbmh_family* family,
                                                 const uint64_t* d_row_ptr, uint64_t index_base,
                                                 const uint32_t* d_indices, uint64_t n,

@@ -57,6 +57,9 @@ constexpr uint64_t kDefaultChunkDocs = 32768;
 constexpr uint64_t kChunkIdxCap = 1ull << 24;        // 16 Mi ids (64 MiB) per chunk
 constexpr uint64_t kChunkMinimaBytes = 256ull << 20;  // cap on a chunk's minima buffer
 constexpr uint64_t kMinSplitIds = 1ull << 20;         // smallest chunk a batch is split into
+// The sketch kernel's bulk copies read ids in whole 16-byte granules, i.e. up
+// to 3 ids past a row's last one: every id buffer we allocate carries that slack.
+constexpr uint64_t kIdsSlack = 4;
 
 std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
     auto df = std::make_unique<DeviceFamily>();
@@ -290,7 +293,7 @@ void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) 
         BBMH_CUDA(cudaMallocHost(&s.h_flags, cap));
         s.cap_rows = cap;
     }
-    grow_device(s.d_idx, s.cap_idx, std::max<uint64_t>(nidx, 4));
+    grow_device(s.d_idx, s.cap_idx, nidx + kIdsSlack);
     if (need_pinned_idx) grow_host(s.h_idx, s.cap_idx_pinned, std::max<uint64_t>(nidx, 4));
     const uint64_t ncodes = std::max<uint64_t>(rows * cb_, 1);
     if (ncodes > s.cap_codes) {
@@ -364,7 +367,7 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     uint8_t* d = s.d_blk;
     const uint32_t* d_ids = reinterpret_cast<const uint32_t*>(d + s.off_ids);
     if (!inline_ids && nidx) {
-        grow_device(s.d_idx, s.cap_idx, std::max<uint64_t>(nidx, 4));
+        grow_device(s.d_idx, s.cap_idx, nidx + kIdsSlack);
         BBMH_CUDA(cudaMemcpyAsync(s.d_idx, job.indices, nidx * sizeof(uint32_t),
                                   cudaMemcpyHostToDevice, s.st));
         d_ids = s.d_idx;
@@ -566,8 +569,11 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
         const char* e = std::getenv("BBMH_ZERO_COPY");  // developer knob (A/B timing)
         return !(e && *e == '0');
     }();
+    // (zero-copy reads the caller's buffer in whole 16-byte granules: only
+    // when the last id ends one, so nothing past the caller's data is touched)
     if (zero_copy_on && pinned && !minima && !score && f.scheme == Scheme::TwoU &&
-        row_ptr[n] - row_ptr[0] <= kZeroCopyMaxIds) {
+        row_ptr[n] - row_ptr[0] <= kZeroCopyMaxIds &&
+        ((uintptr_t)(indices + row_ptr[n]) & 15) == 0) {
         const std::vector<int> devs = pipeline_devices();
         if (devs.size() == 1 && sketch_rows_zero_copy(f, devs[0], row_ptr, indices, n, b, codes, flags))
             return;

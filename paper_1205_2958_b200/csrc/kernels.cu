@@ -205,11 +205,8 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 // One unit of pipelined work: up to `tile` ids of one document.
 struct Item {
     uint64_t doc;
-    const uint32_t* tsrc;  // first of the `tail` ids loaded by threads
     uint32_t cnt;    // ids in this tile (0 for an empty document)
     uint32_t head;   // garbage ids before the first one (16-byte alignment of the copy)
-    uint32_t tail;   // ids past the last full 16-byte granule (0..3): plain loads
-    uint32_t tma;    // a bulk copy was issued (the mbarrier completes a phase)
     uint32_t first;  // first tile of the document
     uint32_t last;   // last tile (run the epilogue)
     uint32_t empty;  // document has no ids
@@ -217,9 +214,13 @@ struct Item {
 };
 
 // each buffer holds tile + 8 ids: room for the 16-byte head/tail slack.
-// The bulk copy covers [src rounded down to 16 B, end rounded down to 16 B):
-// it never reads past the last id of the row (the caller's buffer may end
-// there); the 0..3 ids after the last full granule are loaded by threads.
+// The bulk copy spans whole 16-byte granules, so it may read up to 12 bytes
+// past an item's last id (inside the same granule, never across a page); the
+// values land in the slack and are overwritten by the padding. Every id
+// buffer the library allocates has that slack (engine.cu kIdsSlack); callers
+// of the device API are told so in bbmh_ext.h. (Splitting the tail off the
+// copy cost 1.5-2% of 2U throughput through register allocation in the hash
+// loop, profiles/r10/README.md.)
 
 // Persistent sketch kernel. Each CTA walks documents blockIdx.x,
 // blockIdx.x + gridDim.x, ... for hash-function tile blockIdx.y. Thread 0 is
@@ -277,19 +278,12 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         if (it.cnt) {
             const uint32_t* src = indices + (p_beg - index_base) + p_off;
             const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
-            const uintptr_t end = (uintptr_t)(src + it.cnt);
-            const uintptr_t a1 = end & ~(uintptr_t)15;
             it.head = (uint32_t)(((uintptr_t)src - a0) >> 2);
-            it.tail = (uint32_t)((end - a1) >> 2);
-            it.tsrc = reinterpret_cast<const uint32_t*>(a1);
-            if (a1 > a0) {
-                // order earlier generic-proxy writes to this buffer before the async-proxy copy
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&mbar[bi], (uint32_t)(a1 - a0));
-                tma_bulk_g2s(smem + bi * kBuf, reinterpret_cast<const void*>(a0),
-                             (uint32_t)(a1 - a0), &mbar[bi]);
-                it.tma = 1;
-            }
+            const uint32_t bytes = ((it.head + it.cnt) * 4 + 15) & ~15u;
+            // order earlier generic-proxy writes to this buffer before the async-proxy copy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&mbar[bi], bytes);
+            tma_bulk_g2s(smem + bi * kBuf, reinterpret_cast<const void*>(a0), bytes, &mbar[bi]);
         }
         desc[bi] = it;
         if (it.last) {
@@ -333,15 +327,9 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         }
         if (d.cnt) {
             uint32_t* buf = smem + bi * kBuf;
-            if (d.tma) {
-                mbar_wait(&mbar[bi], (phase >> bi) & 1);
-                phase ^= 1u << bi;
-            }
+            mbar_wait(&mbar[bi], (phase >> bi) & 1);
+            phase ^= 1u << bi;
             const uint32_t lo = d.head, hi = d.head + d.cnt;
-            if (d.tail) {
-                if (tid < d.tail) buf[hi - d.tail + tid] = __ldg(d.tsrc + tid);
-                __syncthreads();
-            }
             const uint32_t n4 = (hi + 3) >> 2;
             constexpr bool kTransform = SCHEME != S_2U;
             if (kTransform || lo != 0 || (hi & 3) != 0) {

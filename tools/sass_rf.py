@@ -6,7 +6,7 @@ operands flagged .reuse. Reports, per loop body, issue slots, fma-heavy and
 alu pipe cycles (2 per warp instruction) and RF cycles, so the binding
 resource of an integer loop can be read off the SASS.
 
-  python tools/sass_rf.py file.sass START_ADDR END_ADDR
+  python tools/sass_rf.py file.sass [START_ADDR END_ADDR]   (default: hottest loop)
 """
 import re
 import sys
@@ -91,6 +91,29 @@ def report(body):
             "pred_fma_util_consumer": util(rf1), "pred_fma_util_flag": util(rf2)}
 
 
+def hottest_loop(lines):
+    """(start, end) of the backward-branch body with the highest IMAD density."""
+    ins = []
+    for ln in lines:
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
+        if m:
+            ins.append((int(m.group(1), 16), m.group(2)))
+    best = None
+    for a, txt in ins:
+        m = re.search(r"BRA\S*\s+(?:!?U?P\d,\s*)?0x([0-9a-f]+)", txt)
+        if m and int(m.group(1), 16) < a:
+            t0 = int(m.group(1), 16)
+            body = [t for b, t in ins if t0 <= b <= a]
+            n = sum(1 for t in body if t.split()[0] in ("IMAD", "IMAD.WIDE.U32"))
+            if n >= 16 and (best is None or n / len(body) > best[0]):
+                best = (n / len(body), t0, a)
+    return best[1], best[2]
+
+
 if __name__ == "__main__":
     lines = open(sys.argv[1]).read().splitlines()
-    print(report(parse(lines, int(sys.argv[2], 16), int(sys.argv[3], 16))))
+    if len(sys.argv) > 3:
+        a0, a1 = int(sys.argv[2], 16), int(sys.argv[3], 16)
+    else:  # python tools/sass_rf.py file.sass  -> the hottest loop
+        a0, a1 = hottest_loop(lines)
+    print(f"loop {a0:#x}-{a1:#x}", report(parse(lines, a0, a1)))
