@@ -49,6 +49,7 @@ private:
 // Developer tracing: with BBMH_TRACE=1 in the environment, prints
 // "bbmh-trace <ms since first call> <what>" to stderr (pipeline stage timing).
 void trace(const char* what);
+bool trace_on();
 
 // ---- counter-based PRNG (src/prng.hpp:10-61), bit-exact ------------------
 constexpr uint64_t mix64(uint64_t x) {

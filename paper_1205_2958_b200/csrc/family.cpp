@@ -20,12 +20,16 @@
 
 namespace bbmh {
 
-void trace(const char* what) {
+bool trace_on() {
     static const bool on = [] {
         const char* e = std::getenv("BBMH_TRACE");
         return e && *e && *e != '0';
     }();
-    if (!on) return;
+    return on;
+}
+
+void trace(const char* what) {
+    if (!trace_on()) return;
     static const auto t0 = std::chrono::steady_clock::now();
     const double ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -14,6 +14,7 @@
 //     same strtod/strtoll calls the reference makes, so accepted inputs,
 //     values and error texts are identical.
 #include "io.hpp"
+#include "parse.hpp"
 
 #include <cuda_runtime.h>
 #include <fcntl.h>
@@ -24,6 +25,7 @@
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <thread>
 
 namespace bbmh {
@@ -277,20 +279,122 @@ bool parse_line(const char* line, uint64_t line_no, std::vector<uint32_t>& ids, 
     return true;
 }
 
+// Text buffer: page-locked when the GPU parser is used (so blocks DMA straight
+// to the device), plain heap memory otherwise. resize() keeps the contents.
+class TextBuf {
+public:
+    ~TextBuf() { release(); }
+    void set_pinned(bool on) { pinned_ = on; }
+    char* data() { return p_; }
+    size_t size() const { return n_; }
+    char& operator[](size_t i) { return p_[i]; }
+    void resize(size_t n) {
+        if (n <= n_) return;
+        char* q = nullptr;
+        if (pinned_) {
+            if (cudaMallocHost(&q, n) != cudaSuccess) {
+                cudaGetLastError();
+                fail(Errc::Cuda, "cudaMallocHost failed for the text buffer");
+            }
+        } else {
+            q = static_cast<char*>(std::malloc(n));
+            if (!q) fail(Errc::Io, "out of memory");
+        }
+        if (p_) std::memcpy(q, p_, n_);
+        release();
+        p_ = q;
+        n_ = n;
+    }
+
+private:
+    void release() {
+        if (!p_) return;
+        if (pinned_) cudaFreeHost(p_);
+        else std::free(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    char* p_ = nullptr;
+    size_t n_ = 0;
+    bool pinned_ = false;
+};
+
+// Reader resources are pooled process-wide: a 128 MB page-locked text buffer
+// and the device parser's buffers cost tens of milliseconds to allocate, more
+// than parsing a small corpus takes.
+struct TextRes {
+    int device = -1;  // -1: CPU parsing only (plain heap buffer)
+    TextBuf buf;
+    std::unique_ptr<GpuLibsvmParser> gpu;
+};
+std::mutex g_text_mu;
+std::vector<std::unique_ptr<TextRes>> g_text_pool;
+
+std::unique_ptr<TextRes> lease_text_res(int device) {
+    {
+        std::lock_guard lk(g_text_mu);
+        for (size_t i = 0; i < g_text_pool.size(); ++i)
+            if (g_text_pool[i]->device == device) {
+                auto r = std::move(g_text_pool[i]);
+                g_text_pool.erase(g_text_pool.begin() + long(i));
+                return r;
+            }
+    }
+    auto r = std::make_unique<TextRes>();
+    if (device >= 0) {
+        try {
+            r->gpu = std::make_unique<GpuLibsvmParser>(device);
+            r->device = device;
+        } catch (...) {
+            r->gpu.reset();
+        }
+        cudaGetLastError();
+    }
+    r->buf.set_pinned(r->gpu != nullptr);
+    return r;
+}
+
+void return_text_res(std::unique_ptr<TextRes> r) {
+    if (!r) return;
+    std::lock_guard lk(g_text_mu);
+    g_text_pool.push_back(std::move(r));
+}
+
 class LibsvmReader : public CorpusReader {
 public:
     LibsvmReader(const std::string& path, unsigned threads, bool binary)
         : path_(path), threads_(std::max(1u, std::min(threads, 64u))), binary_(binary) {
         f_ = open_or_fail(path, "rb");
-        buf_.resize(kBlock + 1);
+        // the device parser takes binary-mode corpora (the sketch loader)
+        int dev = -1;
+        if (binary_ && gpu_parse_enabled()) {
+            if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+            cudaGetLastError();
+        }
+        res_ = lease_text_res(dev);
+        buf_ = &res_->buf;
+        gpu_ = res_->gpu.get();
+        gpu_block_ = gpu_parse_block_bytes(kGpuBlock);
+        buf_->resize(2 * kBlock + 1);
     }
     ~LibsvmReader() override {
         if (f_) std::fclose(f_);
+        return_text_res(std::move(res_));
     }
 
     bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) override {
         bool any = false;
         while (b.n < max_docs && (b.nids() < max_ids || b.n == 0)) {
+            if (gpu_ && pos_ >= cpu_until_) {
+                const uint64_t n0 = b.n;
+                const int g = gpu_block(b, max_docs, max_ids);
+                if (g == 1) {
+                    any |= b.n > n0;
+                    continue;
+                }
+                if (g == 0 || g == 2) break;  // end of input / batch full
+                // g < 0: the block is parsed by the CPU path below
+            }
             // gather complete lines (as NUL-terminated spans) for this round
             std::vector<std::pair<size_t, size_t>> lines;  // [begin, end) in buf_
             const uint64_t byte_budget = std::max<uint64_t>(1, (max_ids - std::min(max_ids, b.nids())) * 4);
@@ -308,21 +412,97 @@ public:
 
 private:
     static constexpr size_t kBlock = size_t(64) << 20;
+    static constexpr size_t kGpuBlock = size_t(32) << 20;
+
+    // One block of complete lines through the GPU parser. Returns 1 if the
+    // block was consumed, 0 at the end of input, 2 if it does not fit the
+    // batch (it starts the next one), -1 if it must go through the CPU parser
+    // (set up via cpu_until_).
+    int gpu_block(Batch& b, uint64_t max_docs, uint64_t max_ids) {
+        const uint64_t rows_left = max_docs - b.n;
+        // size the block from the bytes per line / per id seen so far so its
+        // rows and ids fit the batch; when less than ~2 lines' worth is left,
+        // the batch is full and the block starts the next one
+        size_t target = gpu_block_;
+        if (lines_seen_) {
+            const double per_line = double(bytes_seen_) / double(lines_seen_);
+            const double per_id = ids_seen_ ? double(bytes_seen_) / double(ids_seen_) : 4.0;
+            const uint64_t ids_left = max_ids > b.nids() ? max_ids - b.nids() : 0;
+            double fit = 0.9 * per_line * double(rows_left);
+            if (b.n > 0) fit = std::min(fit, 0.9 * per_id * double(ids_left));
+            if (b.n > 0 && fit < 2 * per_line) return 2;
+            if (fit < double(target)) target = std::max<size_t>(4096, size_t(fit));
+        }
+        for (;;) {
+            if (len_ - pos_ < target && !eof_) {
+                trace("reader: refill");
+                refill();
+                trace("reader: refilled");
+                continue;
+            }
+            if (pos_ >= len_) return 0;
+            const size_t end = std::min(len_, pos_ + target);
+            size_t cut = 0;
+            if (end == len_ && eof_) {
+                cut = len_;
+            } else {
+                const void* nl = memrchr(buf_->data() + pos_, '\n', end - pos_);
+                if (nl) cut = size_t(static_cast<const char*>(nl) - buf_->data()) + 1;
+            }
+            if (!cut) {  // one line longer than the block: widen it
+                if (eof_ && end == len_) return 0;
+                target *= 2;
+                continue;
+            }
+            const bool at_eof = cut == len_ && eof_;
+            auto reserve = [&](uint64_t need) {
+                if (need > b.cap_ids) b.reserve_ids(need + (1u << 20));
+                return b.ids;
+            };
+            const GpuParseResult r =
+                gpu_->parse(buf_->data() + pos_, cut - pos_, at_eof, b.nids(), rows_left,
+                            b.n == 0 ? UINT64_MAX : max_ids - std::min(max_ids, b.nids()), reserve,
+                            b.row_ptr, b.labels);
+            if (!r.ok) {
+                if (r.over_budget && b.n > 0) {
+                    trace("reader: batch full");
+                    return 2;  // this block starts the next batch
+                }
+                trace("reader: gpu block declined");
+                cpu_until_ = cut;
+                return -1;
+            }
+            if (trace_on()) {
+                char msg[96];
+                std::snprintf(msg, sizeof msg, "reader: gpu block parsed (%zu bytes, %llu rows)",
+                              size_t(cut - pos_), (unsigned long long)r.rows);
+                trace(msg);
+            }
+            b.n += r.rows;
+            line_no_ += r.lines;
+            lines_seen_ += r.lines;
+            bytes_seen_ += cut - pos_;
+            ids_seen_ += r.ids;
+            pos_ = cut;
+            gpu_blocks_ += 1;
+            return pos_ < len_ || !eof_ || r.rows ? 1 : 0;
+        }
+    }
 
     // Finds the next line starting at pos_; reads more input as needed.
     bool next_line(std::vector<std::pair<size_t, size_t>>& lines) {
         for (;;) {
-            void* nl = pos_ < len_ ? std::memchr(buf_.data() + pos_, '\n', len_ - pos_) : nullptr;
+            void* nl = pos_ < len_ ? std::memchr(buf_->data() + pos_, '\n', len_ - pos_) : nullptr;
             if (nl) {
-                const size_t e = size_t(static_cast<char*>(nl) - buf_.data());
-                buf_[e] = '\0';
+                const size_t e = size_t(static_cast<char*>(nl) - buf_->data());
+                (*buf_)[e] = '\0';
                 lines.emplace_back(pos_, e);
                 pos_ = e + 1;
                 return true;
             }
             if (eof_) {
                 if (pos_ < len_) {  // last line without a newline
-                    buf_[len_] = '\0';
+                    (*buf_)[len_] = '\0';
                     lines.emplace_back(pos_, len_);
                     pos_ = len_;
                     return true;
@@ -336,21 +516,59 @@ private:
 
     void refill() {
         if (pos_ > 0) {
-            std::memmove(buf_.data(), buf_.data() + pos_, len_ - pos_);
+            std::memmove(buf_->data(), buf_->data() + pos_, len_ - pos_);
             len_ -= pos_;
+            cpu_until_ = cpu_until_ > pos_ ? cpu_until_ - pos_ : 0;
             pos_ = 0;
         }
-        if (len_ + kBlock / 2 > buf_.size() - 1) buf_.resize(std::max(buf_.size() * 2, len_ + kBlock + 1));
-        const size_t want = buf_.size() - 1 - len_;
-        const size_t got = std::fread(buf_.data() + len_, 1, want, f_);
-        if (got < want) {
-            if (std::ferror(f_)) fail(Errc::Io, path_ + ": read error");
-            eof_ = true;
-        }
+        if (len_ + kBlock / 2 > buf_->size() - 1) buf_->resize(std::max(buf_->size() * 2, len_ + kBlock + 1));
+        const size_t want = buf_->size() - 1 - len_;
+        const size_t got = read_at(buf_->data() + len_, want);
+        if (got < want) eof_ = true;
         len_ += got;
     }
 
     void compact_if_needed() {}
+
+    // pread of [file_off_, file_off_ + n) into p, split over up to 8 threads
+    // (one thread copies ~10 GB/s out of the page cache); returns bytes read.
+    size_t read_at(char* p, size_t n) {
+        const int fd = fileno(f_);
+        const unsigned T = n >= (size_t(16) << 20) ? std::min(8u, threads_) : 1u;
+        std::vector<size_t> got(T, 0);
+        std::vector<int> err(T, 0);
+        auto work = [&](unsigned w) {
+            const size_t lo = n * w / T, hi = n * (w + 1) / T;
+            size_t done = 0;
+            while (lo + done < hi) {
+                const ssize_t r = ::pread(fd, p + lo + done, hi - lo - done, off_t(file_off_ + lo + done));
+                if (r < 0) {
+                    if (errno == EINTR) continue;
+                    err[w] = errno;
+                    break;
+                }
+                if (r == 0) break;
+                done += size_t(r);
+            }
+            got[w] = done;
+        };
+        if (T == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> ts;
+            for (unsigned w = 1; w < T; ++w) ts.emplace_back(work, w);
+            work(0);
+            for (auto& t : ts) t.join();
+        }
+        size_t total = 0;
+        for (unsigned w = 0; w < T; ++w) {
+            if (err[w]) fail(Errc::Io, path_ + ": read error");
+            total += got[w];
+            if (got[w] < n * (w + 1) / T - n * w / T) break;  // end of file inside slice w
+        }
+        file_off_ += total;
+        return total;
+    }
 
     struct Frag {
         std::vector<uint32_t> ids;
@@ -375,7 +593,7 @@ private:
                 if (s == e) continue;  // blank line: skipped, but numbered
                 int8_t label = 1;
                 const size_t before = fr.ids.size();
-                if (!parse_line(buf_.data() + s, line0 + i + 1, fr.ids, label, fr.err,
+                if (!parse_line(buf_->data() + s, line0 + i + 1, fr.ids, label, fr.err,
                                 binary_ ? nullptr : &fr.vals)) {
                     fr.err_line = i;
                     fr.ids.resize(before);
@@ -418,10 +636,16 @@ private:
     unsigned threads_;
     bool binary_;
     FILE* f_ = nullptr;
-    std::vector<char> buf_;
+    std::unique_ptr<TextRes> res_;  // pooled: pinned text buffer + device parser
+    TextBuf* buf_ = nullptr;
+    uint64_t file_off_ = 0;  // bytes of the file consumed by read_at
     size_t pos_ = 0, len_ = 0;
     bool eof_ = false;
     uint64_t line_no_ = 0;
+    GpuLibsvmParser* gpu_ = nullptr;
+    size_t cpu_until_ = 0;  // buffer offset up to which lines go through the CPU parser
+    uint64_t lines_seen_ = 0, bytes_seen_ = 0, ids_seen_ = 0, gpu_blocks_ = 0;
+    size_t gpu_block_ = kGpuBlock;
 };
 
 }  // namespace

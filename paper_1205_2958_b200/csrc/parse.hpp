@@ -1,0 +1,84 @@
+// parse.hpp -- LibSVM text -> CSR on the GPU (the loader's fast path).
+//
+// The reference parses one line at a time with strtod/strtoll on one thread
+// (parse_libsvm, dataio.cpp:60-106; LibsvmSource::next, :157-190). Here a
+// whole block of complete lines is copied to the device and split, tokenised
+// and converted by byte-parallel kernels. Only a strict subset of the grammar
+// is accepted on the device -- every line "L( SEP I:1)* SEP* CR?" with
+// L in {+1,-1,1,0,+0,-0}, SEP in {' ','\t'}, I a decimal in [1, 2^32-1],
+// ids strictly ascending, no '#'. A block with anything else (comments,
+// other spellings of numbers, errors) is reported as not parsed and the
+// caller parses it with the CPU parser, which reproduces the reference's
+// values, line numbers and messages exactly.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+namespace bbmh {
+
+struct GpuParseResult {
+    bool ok = false;           // false: the block must be parsed on the CPU
+    bool over_budget = false;  // declined only because it holds more than max_rows / max_ids
+    uint64_t lines = 0;        // lines consumed (blank ones included)
+    uint64_t rows = 0;         // non-blank lines
+    uint64_t ids = 0;          // ids written
+};
+
+class GpuLibsvmParser {
+public:
+    explicit GpuLibsvmParser(int device);
+    ~GpuLibsvmParser();
+    GpuLibsvmParser(const GpuLibsvmParser&) = delete;
+    GpuLibsvmParser& operator=(const GpuLibsvmParser&) = delete;
+
+    // `text` (page-locked) holds complete lines: it ends with '\n', or is the
+    // end of the file (`at_eof`). On success the rows are appended: ids (0-based)
+    // to ids_out (capacity checked through `reserve`, which may move it),
+    // row ends (offset by `id_base`) to row_ptr, labels to labels. At most
+    // max_rows rows and max_ids ids are accepted; a larger block is declined.
+    template <typename Reserve>
+    GpuParseResult parse(const char* text, uint64_t len, bool at_eof, uint64_t id_base,
+                         uint64_t max_rows, uint64_t max_ids, Reserve&& reserve,
+                         std::vector<uint64_t>& row_ptr, std::vector<int8_t>& labels) {
+        GpuParseResult r = run(text, len, at_eof, max_rows, max_ids);
+        if (!r.ok) return r;
+        uint32_t* ids_out = reserve(id_base + r.ids);
+        fetch(ids_out + id_base, id_base, row_ptr, labels, r);
+        return r;
+    }
+
+private:
+    GpuParseResult run(const char* text, uint64_t len, bool at_eof, uint64_t max_rows,
+                       uint64_t max_ids);
+    void fetch(uint32_t* ids_out, uint64_t id_base, std::vector<uint64_t>& row_ptr,
+               std::vector<int8_t>& labels, const GpuParseResult& r);
+    void grow(uint64_t len);
+
+    int device_ = 0;
+    cudaStream_t st_ = nullptr;
+    uint64_t cap_text_ = 0, cap_seg_ = 0, cap_lines_ = 0, cap_ids_ = 0;
+    char* d_text_ = nullptr;
+    unsigned long long* d_seg_ = nullptr;   // per segment: newlines << 32 | colons, then scanned
+    uint64_t* d_line_end_ = nullptr;        // position of each line's '\n' (or len)
+    uint32_t* d_colons_before_ = nullptr;   // ids before each line start (lines + 1)
+    uint32_t* d_line_tok_ = nullptr;        // tokens per line
+    uint32_t* d_row_of_line_ = nullptr;     // 1 for non-blank lines, then scanned
+    int8_t* d_line_label_ = nullptr;
+    uint32_t* d_ids_ = nullptr;
+    uint64_t* d_row_end_ = nullptr;         // rows: end (exclusive) in ids
+    int8_t* d_labels_ = nullptr;
+    uint32_t* d_flags_ = nullptr;           // [0] bad, [1] rows
+    uint32_t* h_flags_ = nullptr;           // pinned mirror
+    void* d_scan_tmp_ = nullptr;
+    size_t scan_tmp_bytes_ = 0;
+};
+
+// BBMH_GPU_PARSE=0 disables the device parser (CPU parsing only); read when a
+// reader is opened. BBMH_GPU_PARSE_BLOCK=<bytes> overrides the block size.
+bool gpu_parse_enabled();
+uint64_t gpu_parse_block_bytes(uint64_t dflt);
+
+}  // namespace bbmh
