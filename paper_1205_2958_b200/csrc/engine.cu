@@ -65,7 +65,13 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
     auto df = std::make_unique<DeviceFamily>();
     df->device = device;
     KernelFamily& kf = df->kf;
-    kf.scheme = int32_t(f.scheme);
+    // 4U-mod with the Mersenne prime (the default, capi.cpp:137) computes the
+    // same residues as 4U-bit (hash_family.hpp:84-87 vs 24-32, SURVEY App. B:
+    // 0 mismatches), so it runs the shift-add kernel: strength reduction of
+    // `% p`, bit-identical output. Other primes keep the Barrett kernel.
+    const Scheme scheme =
+        f.scheme == Scheme::FourUMod && f.p == kMersenne31 ? Scheme::FourUBit : f.scheme;
+    kf.scheme = int32_t(scheme);
     kf.k = f.k;
     kf.dim = f.dim;
     kf.shift2u = f.s >= 32 ? 0 : ((32 - f.s) & 31);  // see Family::map
@@ -75,7 +81,7 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
     kf.neg_dim32 = 0u - uint32_t(f.dim);
     kf.p = uint32_t(f.p);
     kf.barrett = f.p ? (~0ull) / f.p : 0;
-    if (f.scheme == Scheme::FourUBit || f.scheme == Scheme::FourUMod) {
+    if (scheme == Scheme::FourUBit || scheme == Scheme::FourUMod) {
         if (!f.dim_pow2) {
             MagicDiv md = make_magic31(f.dim);
             if (!md.ok) fail(Errc::Cuda, "no 31-bit magic divisor for dim " + std::to_string(f.dim));
@@ -84,7 +90,7 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
         }
     }
     std::vector<uint32_t> coef;
-    switch (f.scheme) {
+    switch (scheme) {
         case Scheme::TwoU:
             coef = f.twou;
             break;

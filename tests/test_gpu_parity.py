@@ -295,3 +295,23 @@ def test_config1_full_size_digests(bb, ref, golden, tmp_path):
         stats = f.sketch_file(corpus, out, c1["b"], 10000, 4, False)
         assert stats["records"] == 20000
         assert hashlib.sha256(open(out, "rb").read()).hexdigest() == digest, scheme
+
+
+@pytest.mark.parametrize("dim", [16609143, 1 << 24, 1010017424, 3, M31 - 1])
+@pytest.mark.parametrize("prime", [0, M31])
+def test_4u_mod_mersenne_runs_the_fold_kernel(bb, port, dim, prime):
+    """4U-mod with p = 2^31 - 1 (the default) is dispatched to the shift-add
+    4U-bit kernel; its output must stay the reference's 4U-mod output."""
+    rng = np.random.default_rng(dim % 1000 + prime % 7)
+    rp, idx = random_csr(rng, 40, min(dim, 1 << 32), 0, 900, empty_every=9)
+    for k, b in ((500, 8), (33, 13), (1, 1)):
+        f = bb.Family(2, dim, k, 77, prime)
+        codes, minima, flags = f.sketch_csr(rp, idx, b, want_minima=True)
+        st, h = port.family(2, dim, k, 77, prime, 0)
+        assert st == 0
+        s, c2, m2, f2 = port.sketch_csr(h, k, rp, idx, b)
+        port.destroy(h)
+        assert s == 0
+        assert np.array_equal(codes, c2) and np.array_equal(minima, m2), (dim, prime, k, b)
+        assert np.array_equal(flags, f2)
+        f.close()
