@@ -25,6 +25,7 @@
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <thread>
 
@@ -375,7 +376,9 @@ public:
         buf_ = &res_->buf;
         gpu_ = res_->gpu.get();
         gpu_block_ = gpu_parse_block_bytes(kGpuBlock);
-        buf_->resize(2 * kBlock + 1);
+        // GPU mode: room for the block being parsed, the read-ahead block and
+        // several more, so the window slides before it has to be compacted
+        buf_->resize(gpu_ ? std::max(2 * kBlock, 8 * gpu_block_) + 1 : 2 * kBlock + 1);
     }
     ~LibsvmReader() override {
         if (f_) std::fclose(f_);
@@ -459,10 +462,35 @@ private:
                 if (need > b.cap_ids) b.reserve_ids(need + (1u << 20));
                 return b.ids;
             };
-            const GpuParseResult r =
-                gpu_->parse(buf_->data() + pos_, cut - pos_, at_eof, b.nids(), rows_left,
-                            b.n == 0 ? UINT64_MAX : max_ids - std::min(max_ids, b.nids()), reserve,
-                            b.row_ptr, b.labels);
+            // read ahead into the free tail of the buffer while the GPU parses
+            // [pos_, cut): disjoint regions, joined before anything moves
+            std::thread ahead;
+            size_t ahead_got = 0;
+            std::exception_ptr ahead_err;
+            if (!eof_ && buf_->size() - 1 - len_ >= gpu_block_) {
+                ahead = std::thread([&] {
+                    try {
+                        ahead_got = read_at(buf_->data() + len_, gpu_block_);
+                    } catch (...) {
+                        ahead_err = std::current_exception();
+                    }
+                });
+            }
+            GpuParseResult r;
+            try {
+                r = gpu_->parse(buf_->data() + pos_, cut - pos_, at_eof, b.nids(), rows_left,
+                                b.n == 0 ? UINT64_MAX : max_ids - std::min(max_ids, b.nids()),
+                                reserve, b.row_ptr, b.labels);
+            } catch (...) {
+                if (ahead.joinable()) ahead.join();
+                throw;
+            }
+            if (ahead.joinable()) {
+                ahead.join();
+                if (ahead_err) std::rethrow_exception(ahead_err);
+                len_ += ahead_got;
+                if (ahead_got < gpu_block_) eof_ = true;
+            }
             if (!r.ok) {
                 if (r.over_budget && b.n > 0) {
                     trace("reader: batch full");
@@ -522,7 +550,8 @@ private:
             pos_ = 0;
         }
         if (len_ + kBlock / 2 > buf_->size() - 1) buf_->resize(std::max(buf_->size() * 2, len_ + kBlock + 1));
-        const size_t want = buf_->size() - 1 - len_;
+        size_t want = buf_->size() - 1 - len_;
+        if (gpu_) want = std::min(want, std::max(gpu_block_, size_t(1) << 20));  // rest: read-ahead
         const size_t got = read_at(buf_->data() + len_, want);
         if (got < want) eof_ = true;
         len_ += got;
