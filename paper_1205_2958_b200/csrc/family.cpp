@@ -79,9 +79,24 @@ void build_perm_tables(Family& f) {
             uint32_t* tab = f.perm.data() + size_t(j) * dim;
             for (uint64_t t = 0; t < dim; ++t) tab[t] = uint32_t(t);
             SplitMix64 rng{keyed_u64(f.seed, rngtag::kPermutation, j, 0)};
-            for (uint64_t t = dim - 1; t > 0; --t) {  // hash_family.cpp:108-112
-                uint64_t r = rng.next_below(t + 1);
+            // hash_family.cpp:108-112, the same draws and swaps in the same
+            // order; the draws run kAhead steps ahead of the swaps so the
+            // random entry each swap touches is prefetched (the shuffle is
+            // bound by cache misses into the 64 MB table otherwise)
+            constexpr uint64_t kAhead = 32;
+            uint64_t ring[kAhead];
+            uint64_t t_draw = dim - 1;  // next t whose r is drawn
+            auto draw = [&] {
+                const uint64_t r = rng.next_below(t_draw + 1);
+                ring[t_draw % kAhead] = r;
+                __builtin_prefetch(tab + r, 1, 0);
+                --t_draw;
+            };
+            for (uint64_t i = 0; i < kAhead && t_draw > 0; ++i) draw();
+            for (uint64_t t = dim - 1; t > 0; --t) {
+                const uint64_t r = ring[t % kAhead];
                 std::swap(tab[t], tab[r]);
+                if (t_draw > 0) draw();
             }
         }
     };
