@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kTpb) seg_emit(const char* __restrict__ t, uin
     before += blockIdx.x ? seg[blockIdx.x - 1] : 0ull;
     uint32_t line = uint32_t(before >> 32), col = uint32_t(before);
     if (chunk == 0) colons_before[0] = 0;
-    char prev = p0 ? t[p0 - 1] : '\n';
+    char prev = p0 && p0 <= len ? t[p0 - 1] : '\n';  // chunks past the end read nothing
     uint32_t tok = 0;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {

@@ -2,7 +2,8 @@
 (memcheck / racecheck / synccheck / initcheck): sketch (2U, 4U-bit with
 power-of-two and general D, 4U-mod, permutation in both schedules, k
 spanning several CTAs, rows longer than one shared-memory tile, empty rows),
-the file pipeline + expansion to BBCV and LibSVM text, fused scoring,
+the file pipeline on BBCV and on LibSVM text (GPU parser + CPU fallback),
+expansion to BBCV and LibSVM text, fused scoring,
 predict on a BBMH file, all-pairs match counts and the VW projection.
 No torch; ctypes only. Usage: compute-sanitizer --tool memcheck python
 tools/sanitize_driver.py"""
@@ -45,6 +46,14 @@ def main():
         sk = os.path.join(td, "c.bbmh")
         with bbmh.Family(1, 1 << 20, 30, 42) as f:
             f.sketch_file(corpus, sk, 4, 5, 2)
+            # LibSVM text: the GPU parser (small blocks) and its CPU fallback
+            txt = os.path.join(td, "c.txt")
+            lines = ["%+d" % lab + "".join(" %d:1" % (t + 1) for t in ids) for lab, ids in rows]
+            open(txt, "w").write("\n".join(lines) + "\n\n0\n+1 5:1 # c\n")
+            os.environ["BBMH_GPU_PARSE_BLOCK"] = "4096"
+            f.sketch_file(txt, os.path.join(td, "t.bbmh"), 4, 5, 2)
+            os.environ.pop("BBMH_GPU_PARSE_BLOCK")
+            f.sketch_file(txt, os.path.join(td, "t2.bbmh"), 4, 5, 2)
         bbmh.expand_file(sk, os.path.join(td, "e.txt"), bbmh.ROWS_LIBSVM)
         bbmh.expand_file(sk, os.path.join(td, "e.bbcv"), bbmh.ROWS_BINARY)
         model = os.path.join(td, "m.bblm")
