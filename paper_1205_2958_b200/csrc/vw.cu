@@ -19,6 +19,10 @@
 #include <cmath>
 #include <cstring>
 #include <cub/cub.cuh>
+#include <algorithm>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
@@ -81,6 +85,25 @@ __global__ void vw_flag_kernel(const int* __restrict__ sums, const int* __restri
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         flags[i] = sums[i] != 0;
 }
+
+// page-locked host array (D2H at full PCIe rate, no zero-fill of a std::vector)
+template <typename T>
+struct HostBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = std::max<size_t>(n, cap + cap / 2);
+        BBMH_CUDA(cudaMallocHost(&p, cap * sizeof(T)));
+    }
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
+};
 
 template <typename T>
 struct Buf {
@@ -152,17 +175,69 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         cudaStream_t s;
         ~SG() { cudaStreamDestroy(s); }
     } sg{st};
-    Buf<uint64_t> d_rp;
-    Buf<uint32_t> d_ids;
-    Buf<unsigned long long> d_keys, d_keys2, d_ukeys, d_okeys;
-    Buf<int> d_vals, d_vals2, d_sums, d_osums, d_nrun, d_nsel, d_err;
-    Buf<unsigned char> d_flags, d_tmp;
+    // device work buffers are kept across calls too (per device; the
+    // function-level lock below serialises their use)
+    struct DevBufs {
+        Buf<uint64_t> d_rp;
+        Buf<uint32_t> d_ids;
+        Buf<unsigned long long> d_keys, d_keys2, d_ukeys, d_okeys;
+        Buf<int> d_vals, d_vals2, d_sums, d_osums, d_nrun, d_nsel, d_err;
+        Buf<unsigned char> d_flags, d_tmp;
+    };
+    static std::mutex dev_mu;
+    static std::vector<std::unique_ptr<DevBufs>> dev_bufs;
+    std::lock_guard dev_lk(dev_mu);
+    {
+        int cur = 0;
+        BBMH_CUDA(cudaGetDevice(&cur));
+        if (size_t(cur) >= dev_bufs.size()) dev_bufs.resize(cur + 1);
+        if (!dev_bufs[cur]) dev_bufs[cur] = std::make_unique<DevBufs>();
+    }
+    int cur_dev = 0;
+    BBMH_CUDA(cudaGetDevice(&cur_dev));
+    DevBufs& D = *dev_bufs[cur_dev];
+    auto& d_rp = D.d_rp;
+    auto& d_ids = D.d_ids;
+    auto& d_keys = D.d_keys;
+    auto& d_keys2 = D.d_keys2;
+    auto& d_ukeys = D.d_ukeys;
+    auto& d_okeys = D.d_okeys;
+    auto& d_vals = D.d_vals;
+    auto& d_vals2 = D.d_vals2;
+    auto& d_sums = D.d_sums;
+    auto& d_osums = D.d_osums;
+    auto& d_nrun = D.d_nrun;
+    auto& d_nsel = D.d_nsel;
+    auto& d_err = D.d_err;
+    auto& d_flags = D.d_flags;
+    auto& d_tmp = D.d_tmp;
     d_nrun.reserve(1);
     d_nsel.reserve(1);
     d_err.reserve(1);
-    std::vector<unsigned long long> keys;
-    std::vector<int> sums;
-    std::string text;
+    {
+        // one allocation round for the largest batch (growing buffers batch by
+        // batch re-allocates, and cudaFree stalls)
+        const size_t cap = (1u << 24) + (1u << 22);
+        d_ids.reserve(cap);
+        d_keys.reserve(cap);
+        d_keys2.reserve(cap);
+        d_vals.reserve(cap);
+        d_vals2.reserve(cap);
+        d_ukeys.reserve(cap);
+        d_sums.reserve(cap);
+        d_okeys.reserve(cap);
+        d_osums.reserve(cap);
+        d_flags.reserve(cap);
+        d_rp.reserve((1u << 16) + 1);
+    }
+    // page-locked result buffers are kept across calls (pinning ~200 MB costs
+    // far more than a batch); calls are serialised on them
+    static std::mutex host_mu;
+    static HostBuf<unsigned long long> keys;
+    static HostBuf<int> sums;
+    std::lock_guard host_lk(host_mu);
+    keys.reserve((1u << 24) + (1u << 22));
+    sums.reserve((1u << 24) + (1u << 22));
     Batch batch;
     uint64_t rows_written = 0;
     int dev = 0, sms = 148;
@@ -172,7 +247,9 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
     for (;;) {
         batch.clear();
         batch.reserve_ids((1u << 24) + (1u << 22));
+        trace("vw: fill");
         if (!reader->fill(batch, 1u << 16, 1u << 24)) break;
+        trace("vw: filled");
         const uint64_t n = batch.n, nid = batch.nids();
         int nsel = 0;
         if (nid) {
@@ -229,42 +306,62 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
             BBMH_CUDA(cudaStreamSynchronize(st));
             if (err)
                 fail(Errc::UnsupportedUniverse, "feature id must be < 2^31-1 for the sign hash");
-            keys.resize(nsel);
-            sums.resize(nsel);
+            keys.reserve(size_t(nsel) + 1);
+            sums.reserve(size_t(nsel) + 1);
             if (nsel) {
-                BBMH_CUDA(cudaMemcpyAsync(keys.data(), d_okeys.p, nsel * 8ull, cudaMemcpyDeviceToHost, st));
-                BBMH_CUDA(cudaMemcpyAsync(sums.data(), d_osums.p, nsel * 4ull, cudaMemcpyDeviceToHost, st));
+                BBMH_CUDA(cudaMemcpyAsync(keys.p, d_okeys.p, nsel * 8ull, cudaMemcpyDeviceToHost, st));
+                BBMH_CUDA(cudaMemcpyAsync(sums.p, d_osums.p, nsel * 4ull, cudaMemcpyDeviceToHost, st));
                 BBMH_CUDA(cudaStreamSynchronize(st));
             }
         }
-        // write_libsvm (dataio.cpp:115-125): "%+d" then " %u:%g" per entry
-        text.clear();
-        text.reserve(size_t(nsel) * 12 + n * 4);
-        char buf[64];
-        uint64_t e = 0;
-        for (uint64_t r = 0; r < n; ++r) {
-            const int lab = batch.labels[r];
-            text += lab < 0 ? '-' : '+';
-            char* q = put_uint(buf, uint64_t(lab < 0 ? -lab : lab));
-            text.append(buf, q);
-            for (; e < uint64_t(nsel) && (keys[e] >> 32) == r; ++e) {
-                const uint32_t bin = uint32_t(keys[e]);
-                const int v = sums[e];
-                char* p = buf;
-                *p++ = ' ';
-                p = put_uint(p, uint32_t(bin + 1u));  // "%u" of the u32 index + 1
-                *p++ = ':';
-                if (v > -1000000 && v < 1000000) {  // %g of an integer below 1e6 prints digits
-                    if (v < 0) *p++ = '-';
-                    p = put_uint(p, uint64_t(v < 0 ? -int64_t(v) : v));
-                } else {
-                    p += std::snprintf(p, 32, "%g", double(float(v)));
+        trace("vw: device done");
+        // write_libsvm (dataio.cpp:115-125): "%+d" then " %u:%g" per entry.
+        // Rows are formatted in parallel ranges (the text is ~12 bytes per
+        // entry: this was the single-threaded bottleneck) and written in order.
+        const unsigned T = n < 512 ? 1u : std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        // entry <= 22 chars (" 4294967296:-999999"), row head <= 3 + newline
+        std::vector<std::vector<char>> parts(T);
+        std::vector<size_t> used(T, 0);
+        auto fmt = [&](unsigned w) {
+            const uint64_t r0 = n * w / T, r1 = n * (w + 1) / T;
+            // first entry of row r0: keys are sorted by (row << 32 | bin)
+            uint64_t e = std::lower_bound(keys.p, keys.p + nsel, (unsigned long long)r0 << 32) - keys.p;
+            uint64_t e_end = std::lower_bound(keys.p, keys.p + nsel, (unsigned long long)r1 << 32) - keys.p;
+            std::vector<char>& buf = parts[w];
+            buf.resize((e_end - e) * 24 + (r1 - r0) * 8 + 64);
+            char* p = buf.data();
+            for (uint64_t r = r0; r < r1; ++r) {
+                const int lab = batch.labels[r];
+                *p++ = lab < 0 ? '-' : '+';
+                p = put_uint(p, uint64_t(lab < 0 ? -lab : lab));
+                for (; e < e_end && (keys[e] >> 32) == r; ++e) {
+                    const uint32_t bin = uint32_t(keys[e]);
+                    const int v = sums[e];
+                    *p++ = ' ';
+                    p = put_uint(p, uint32_t(bin + 1u));  // "%u" of the u32 index + 1
+                    *p++ = ':';
+                    if (v > -1000000 && v < 1000000) {  // %g of an integer below 1e6 prints digits
+                        if (v < 0) *p++ = '-';
+                        p = put_uint(p, uint64_t(v < 0 ? -int64_t(v) : v));
+                    } else {
+                        p += std::snprintf(p, 32, "%g", double(float(v)));
+                    }
                 }
-                text.append(buf, p);
+                *p++ = '\n';
             }
-            text += '\n';
+            used[w] = size_t(p - buf.data());
+        };
+        if (T == 1) {
+            fmt(0);
+        } else {
+            std::vector<std::thread> ts;
+            for (unsigned w = 1; w < T; ++w) ts.emplace_back(fmt, w);
+            fmt(0);
+            for (auto& t : ts) t.join();
         }
-        write_all(out, text.data(), text.size());
+        trace("vw: formatted");
+        for (unsigned w = 0; w < T; ++w) write_all(out, parts[w].data(), used[w]);
+        trace("vw: written");
         rows_written += n;
     }
     return rows_written;
