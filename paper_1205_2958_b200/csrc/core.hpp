@@ -128,7 +128,11 @@ struct Family {
     uint64_t p = kMersenne31;
     std::vector<uint32_t> twou;   // k * {a1, a2}      (hash_family.cpp:72-75)
     std::vector<uint64_t> fouru;  // k * {a0,a1,a2,a3} (hash_family.cpp:90-95)
-    std::vector<uint32_t> perm;   // k * dim, table j at [j*dim, (j+1)*dim)
+    std::vector<uint32_t> perm;   // k * dim, table j at [j*dim, (j+1)*dim) (host-built)
+    // tables built on a GPU instead (permgen.cu): they live in device memory
+    // only, owned by that device's DeviceFamily; `perm` stays empty
+    const uint32_t* perm_dev = nullptr;
+    int perm_dev_id = -1;
 
     // host-side single evaluation (bbmh_family_map; hash_family.hpp:77-92)
     uint32_t map(uint32_t j, uint32_t t) const;
@@ -139,6 +143,14 @@ struct Family {
     Family();
     ~Family();
 };
+
+// Permutation tables built on the current GPU (permgen.cu): the same
+// Fisher-Yates draws and swaps as hash_family.cpp:105-114. Returns false
+// (nothing changed) when no GPU / not enough memory; the caller then builds
+// them on the host.
+bool build_perm_tables_gpu(Family& f);
+// One entry of device-resident tables read back (bbmh_family_map).
+uint32_t perm_value_on_device(const Family& f, uint32_t j, uint32_t t);
 
 // src/hash_family.cpp:53-119 (same validation order, codes and messages).
 std::unique_ptr<Family> build_family(Scheme scheme, uint64_t dim, uint32_t k, uint64_t seed,

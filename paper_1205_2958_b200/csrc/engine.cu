@@ -112,7 +112,8 @@ void upload_large(void* dst, const void* src, size_t bytes) {
     BBMH_CUDA(cudaStreamSynchronize(st));
 }
 
-std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
+std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device,
+                                           uint32_t* adopt_perm = nullptr) {
     auto df = std::make_unique<DeviceFamily>();
     df->device = device;
     KernelFamily& kf = df->kf;
@@ -176,9 +177,26 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device) {
         kf.coef = df->d_coef;
     }
     if (f.scheme == Scheme::Permutation) {
-        const size_t bytes = f.perm.size() * sizeof(uint32_t);
-        BBMH_CUDA(cudaMalloc(&df->d_perm, bytes));
-        upload_large(df->d_perm, f.perm.data(), bytes);
+        const size_t bytes = size_t(f.dim) * f.k * sizeof(uint32_t);
+        if (adopt_perm) {  // built in place on this device (permgen.cu)
+            df->d_perm = adopt_perm;
+        } else if (f.perm.empty()) {
+            // device-built tables live on another GPU: copy peer to peer
+            // (NVLink when the devices can reach each other)
+            BBMH_CUDA(cudaMalloc(&df->d_perm, bytes));
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, device, f.perm_dev_id);
+            if (can) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(f.perm_dev_id, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    BBMH_CUDA(e);
+                cudaGetLastError();
+            }
+            BBMH_CUDA(cudaMemcpyPeer(df->d_perm, device, f.perm_dev, f.perm_dev_id, bytes));
+        } else {
+            BBMH_CUDA(cudaMalloc(&df->d_perm, bytes));
+            upload_large(df->d_perm, f.perm.data(), bytes);
+        }
         kf.perm = df->d_perm;
     }
     return df;
@@ -265,6 +283,21 @@ void check_row_ptr(const uint64_t* rp, uint64_t n) {
 }
 
 }  // namespace
+
+void adopt_device_perm(Family& f, int device, uint32_t* d_perm) {
+    std::lock_guard lk(f.dev_mu);
+    if (size_t(device) >= f.dev.size()) f.dev.resize(device + 1);
+    f.dev[device] = upload_family(f, device, d_perm);
+    f.perm_dev = d_perm;
+    f.perm_dev_id = device;
+}
+
+uint32_t perm_value_on_device(const Family& f, uint32_t j, uint32_t t) {
+    DeviceGuard g(f.perm_dev_id);
+    uint32_t v = 0;
+    BBMH_CUDA(cudaMemcpy(&v, f.perm_dev + size_t(j) * f.dim + t, sizeof v, cudaMemcpyDeviceToHost));
+    return v;
+}
 
 const DeviceFamily& device_family(const Family& f, int device) {
     std::lock_guard lk(f.dev_mu);

@@ -27,6 +27,10 @@ struct DeviceFamily {
 
 const DeviceFamily& device_family(const Family& f, int device);
 
+// Registers permutation tables already built in device memory on `device`
+// (ownership passes to that device's DeviceFamily).
+void adopt_device_perm(Family& f, int device, uint32_t* d_perm);
+
 // Devices used by the host-buffer and file pipelines (empty = current device).
 std::vector<int> pipeline_devices();
 void set_pipeline_devices(const std::vector<int>& ids);

@@ -137,7 +137,8 @@ uint32_t Family::map(uint32_t j, uint32_t t) const {
             return reduce_dim(h);
         }
         case Scheme::Permutation:
-            return perm[size_t(j) * dim + t];
+            if (!perm.empty()) return perm[size_t(j) * dim + t];
+            return perm_value_on_device(*this, j, t);
     }
     return 0;
 }
@@ -192,7 +193,7 @@ std::unique_ptr<Family> build_family(Scheme scheme, uint64_t dim, uint32_t k, ui
                 fail(Errc::PermutationTooLarge,
                      "permutation tables need " + std::to_string(dim * k * 4) +
                          " bytes, cap is " + std::to_string(perm_cap_bytes));
-            build_perm_tables(f);
+            if (!build_perm_tables_gpu(f)) build_perm_tables(f);
             break;
         }
     }
