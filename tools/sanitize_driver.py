@@ -39,6 +39,10 @@ def main():
     os.environ["BBMH_PERM_TABLEWISE"] = "0"
     with bbmh.Family(0, 1 << 12, 9, 42) as f:
         f.sketch_csr(rp, idx % (1 << 12), 6)
+    # >= 64 MB of tables: built on the GPU (permgen.cu), read back by map()
+    with bbmh.Family(0, 1 << 20, 17, 42, 0, 1 << 30) as f:
+        f.sketch_csr(rp, idx, 6)
+        assert 0 <= f.map(16, 12345) < (1 << 20)
     with tempfile.TemporaryDirectory() as td:
         rows = [(1 if i % 2 else -1, idx[int(rp[i]):int(rp[i + 1])]) for i in range(12)]
         corpus = os.path.join(td, "c.bbcv")
