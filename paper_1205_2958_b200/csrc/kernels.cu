@@ -407,6 +407,112 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
     }
 }
 
+// ---- small k (<= 32 for 2U, <= 16 for 4U): split the ids across lanes --------
+// With k < 32 the layout above leaves 32 - k lanes of each warp idle and every
+// busy lane walks all ids of the document alone (latency-bound: 2U at k = 1..32
+// ran at 19% of HBM, 4U-bit at 2%). Here every lane holds all k <= J hash
+// functions and takes every 32nd quad of the document's ids, read straight
+// from global memory with 16-byte loads (each id read once, coalesced across
+// the warp); the 32 partial minima per function are merged with shuffles.
+// Each warp sketches its own documents. Same arithmetic and epilogue as
+// sketch_kernel.
+template <int SCHEME, bool POW2, int J>
+__global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
+                                                           const uint64_t* __restrict__ row_ptr,
+                                                           uint64_t index_base,
+                                                           const uint32_t* __restrict__ indices,
+                                                           uint64_t n_docs, uint32_t b,
+                                                           uint8_t* __restrict__ codes,
+                                                           uint64_t* __restrict__ minima,
+                                                           uint8_t* __restrict__ flags, int* err) {
+    __shared__ uint32_t s_code[4][J];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const uint32_t k = Fm.k;
+    Coef<SCHEME> c[J];
+#pragma unroll
+    for (int r = 0; r < J; ++r) c[r].load(Fm, (uint32_t)r < k ? r : k - 1);
+    const uint32_t mask = b >= 32 ? 0xffffffffu : ((1u << b) - 1);
+    const uint64_t cb = ((uint64_t)k * b + 7) >> 3;
+    for (uint64_t doc = (uint64_t)blockIdx.x * W + warp; doc < n_docs;
+         doc += (uint64_t)gridDim.x * W) {
+        uint64_t beg = row_ptr[doc], end = row_ptr[doc + 1];
+        if (end < beg) {
+            if (lane == 0) atomicOr(err, 2);
+            end = beg;
+        }
+        const uint32_t* ids = indices + (beg - index_base);
+        const uint64_t nnz = end - beg;
+        uint32_t m[J];
+#pragma unroll
+        for (int r = 0; r < J; ++r) m[r] = 0xffffffffu;
+        auto eval = [&](uint32_t t) {
+            const uint32_t tt = stage_transform<SCHEME>(Fm, t, err);
+#pragma unroll
+            for (int r = 0; r < J; ++r) m[r] = min(m[r], hash1<SCHEME, POW2>(Fm, c[r], tt));
+        };
+        // head ids up to 16-byte alignment, whole quads, tail ids
+        const uint64_t head = nnz < ((16 - ((uintptr_t)ids & 15)) & 15) / 4
+                                  ? nnz : ((16 - ((uintptr_t)ids & 15)) & 15) / 4;
+        if (lane < head) eval(__ldg(ids + lane));
+        const uint64_t nq = (nnz - head) / 4;
+        const uint4* q4 = reinterpret_cast<const uint4*>(ids + head);
+        for (uint64_t q = lane; q < nq; q += 64) {
+            const uint4 x = __ldg(q4 + q);
+            const bool two = q + 32 < nq;
+            const uint4 y = two ? __ldg(q4 + q + 32) : x;
+            eval(x.x);
+            eval(x.y);
+            eval(x.z);
+            eval(x.w);
+            if (two) {
+                eval(y.x);
+                eval(y.y);
+                eval(y.z);
+                eval(y.w);
+            }
+        }
+        const uint64_t t0 = head + 4 * nq;
+        if (t0 + lane < nnz) eval(__ldg(ids + t0 + lane));
+        // merge the 32 lanes' minima, function by function
+#pragma unroll
+        for (int r = 0; r < J; ++r) {
+#pragma unroll
+            for (uint32_t off = 1; off < 32; off <<= 1)
+                m[r] = min(m[r], __shfl_xor_sync(0xffffffffu, m[r], off));
+            if constexpr (SCHEME == S_2U) m[r] >>= Fm.shift2u;
+        }
+        const bool empty = nnz == 0;
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < J; ++r)
+                if ((uint32_t)r < k) s_code[warp][r] = empty ? mask : (m[r] & mask);
+            if (flags) flags[doc] = empty ? 1 : 0;
+        }
+        if (minima) {
+#pragma unroll
+            for (int r = 0; r < J; ++r)
+                if (lane == (uint32_t)r && (uint32_t)r < k)
+                    minima[doc * k + r] = empty ? ~0ull : (uint64_t)m[r];
+        }
+        __syncwarp();
+        uint8_t* out = codes + doc * cb;
+        for (uint64_t B = lane; B < cb; B += 32) {
+            const uint64_t bit0 = B << 3;
+            const uint32_t ja = (uint32_t)(bit0 / b);
+            const uint64_t jb0 = (bit0 + 7) / b;
+            const uint32_t jb = (uint32_t)(jb0 < k - 1 ? jb0 : k - 1);
+            uint32_t v = 0;
+            for (uint32_t j = ja; j <= jb; ++j) {
+                const uint64_t code = s_code[warp][j];
+                const int64_t pos = (int64_t)j * b - (int64_t)bit0;
+                v |= (uint32_t)(pos >= 0 ? (code << pos) : (code >> -pos));
+            }
+            out[B] = (uint8_t)v;
+        }
+        __syncwarp();
+    }
+}
+
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return v && *v ? std::atoi(v) : dflt;
@@ -481,6 +587,41 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
 }
 
 
+template <int SCHEME, bool POW2, int FF>
+void launch_split(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
+                  const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima,
+                  uint8_t* flags, int* err, cudaStream_t st) {
+    constexpr int kTpb = 128;  // 4 warps, each on its own documents
+    static std::atomic<int> occ_cache{0};
+    int occ = occ_cache.load(std::memory_order_relaxed);
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sketch_split_kernel<SCHEME, POW2, FF>,
+                                                      kTpb, 0);
+        occ = occ < 1 ? 1 : occ;
+        occ_cache.store(occ, std::memory_order_relaxed);
+    }
+    uint64_t grid = (uint64_t)device_sms() * occ;
+    const uint64_t need = (n + 3) / 4;
+    if (grid > need) grid = need;
+    sketch_split_kernel<SCHEME, POW2, FF><<<(unsigned)grid, kTpb, 0, st>>>(
+        F, row_ptr, base, idx, n, b, codes, minima, flags, err);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+template <int SCHEME, bool POW2>
+void dispatch_split(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
+                    const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima,
+                    uint8_t* flags, int* err, cudaStream_t st) {
+    const uint32_t k = F.k;
+    if (k <= 1) return launch_split<SCHEME, POW2, 1>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+    if (k <= 2) return launch_split<SCHEME, POW2, 2>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+    if (k <= 4) return launch_split<SCHEME, POW2, 4>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+    if (k <= 8) return launch_split<SCHEME, POW2, 8>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+    if constexpr (SCHEME == S_2U)
+        if (k > 16) return launch_split<SCHEME, POW2, 32>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+    return launch_split<SCHEME, POW2, 16>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+}
+
 }  // namespace
 
 LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
@@ -534,6 +675,20 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
                    const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima,
                    uint8_t* flags, int* err, cudaStream_t st) {
     if (n == 0) return;
+    const uint32_t split_max = F.scheme == S_2U ? 32u : 16u;  // functions a lane holds in registers
+    if (F.k <= split_max && F.scheme != S_PERM && env_int("BBMH_SPLIT_SMALL_K", 1)) {
+        switch (F.scheme) {
+            case S_2U: return dispatch_split<S_2U, true>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            case S_4UBIT:
+                if (F.dim_pow2)
+                    return dispatch_split<S_4UBIT, true>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+                return dispatch_split<S_4UBIT, false>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            default:
+                if (F.dim_pow2)
+                    return dispatch_split<S_4UMOD, true>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+                return dispatch_split<S_4UMOD, false>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        }
+    }
     const LaunchShape sh = choose_shape(F.k, F.scheme, n, device_sms());
     switch (F.scheme) {
         case S_2U:

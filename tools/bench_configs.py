@@ -12,6 +12,7 @@ Prints one JSON object per line (and writes them to --out):
           b in 1..16, latency p50/p99 through bbmh_ext_sketch_csr
   loader  bbmh_sketch_file on BBCV and LibSVM text corpora: MB/s and the
           read/compute/write split
+  ksweep  which roofline (integer pipes or HBM) binds at k = 1, 8, 32, 200, 500
 Usage: python tools/bench_configs.py [--only c1,c3,...] [--out file.jsonl]
 """
 from __future__ import annotations
@@ -132,6 +133,44 @@ def run_c3(n_docs):
           "sector_bound_gathers_per_s_at_hbm": 6461.2e9 / 32})
     f.close()
     del d_rp, d_idx, d_codes
+    torch.cuda.empty_cache()
+
+
+def run_ksweep(n_docs):
+    """Which roofline binds at k in {1, 8, 32, 200, 500}: kernel
+    throughput on the HBM-resident webspam-shaped corpus, the integer-pipe
+    fraction (measured pipe rates, 1,965 MHz) and the HBM fraction of the
+    algorithmic bytes (ids in, codes + flags out) per launch."""
+    dev = torch.device("cuda", 0)
+    d_rp, d_idx = bench.make_corpus_device(torch, n_docs, bench.NNZ, bench.D_WEBSPAM, 5, dev)
+    peaks = bench.int_peaks()
+    b = 8
+    for scheme, sid, dim in (("2u", 1, 1 << 24), ("4u-bit", 3, bench.D_WEBSPAM)):
+        for k in (1, 8, 32, 200, 500):
+            cb = (k * b + 7) // 8
+            d_codes = torch.empty(n_docs * cb, dtype=torch.uint8, device=dev)
+            d_flags = torch.empty(n_docs, dtype=torch.uint8, device=dev)
+            f = bbmh.Family(sid, dim, k, 42)
+            st = torch.cuda.current_stream()
+            ms = dev_time(lambda: f.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n_docs, b,
+                                                      d_codes.data_ptr(), None, d_flags.data_ptr(),
+                                                      stream=st.cuda_stream), reps=3)
+            evals = n_docs * bench.NNZ * k
+            bytes_ = n_docs * bench.NNZ * 4 + (n_docs + 1) * 8 + n_docs * (cb + 1)
+            rf = bench.roofline_int(scheme, dim, evals / ms * 1e3, 1965.0, peaks)
+            hbm_frac = bytes_ / (ms * 1e-3) / 6461.2e9
+            # time each roofline alone would allow; the larger one binds
+            t_int = evals / (rf["peak"] * 1e9) if rf else None
+            t_hbm = bytes_ / 6461.2e9
+            emit({"config": "ksweep", "scheme": scheme, "k": k, "docs": n_docs, "kernel_ms": ms,
+                  "hash_evals_per_s": evals / ms * 1e3, "docs_per_s": n_docs / ms * 1e3,
+                  "int_frac": rf["frac"] if rf else None, "hbm_gbs": bytes_ / ms / 1e6,
+                  "hbm_frac": hbm_frac,
+                  "predicted_binding": "int" if t_int and t_int > t_hbm else "hbm",
+                  "measured_binding": "int" if rf and rf["frac"] > hbm_frac else "hbm"})
+            f.close()
+            del d_codes, d_flags
+    del d_rp, d_idx
     torch.cuda.empty_cache()
 
 
@@ -337,6 +376,8 @@ def main():
                     run_c3(args.c3_docs)
                 elif what == "c4":
                     run_c4(args.c4_docs)
+                elif what == "ksweep":
+                    run_ksweep(200_000)
                 elif what == "c5":
                     run_c5()
                 elif what == "loader":
