@@ -582,6 +582,10 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
         case 2: return launch_one<SCHEME, POW2, 2>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         case 4: return launch_one<SCHEME, POW2, 4>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         case 8: return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case 7:
+            if constexpr (SCHEME == S_2U)
+                return launch_one<SCHEME, POW2, 7>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         default: return launch_one<SCHEME, POW2, 16>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
     }
 }
@@ -640,9 +644,12 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     const double docs = n ? (double)n : 1e12;
     LaunchShape best;
     double best_cost = 1e300;
-    const int Js[4] = {8, 4, 2, 1};
+    // J = 7 (2U only): 7 x 32 = 224 lanes fit k = 200 (config 1) with 11% idle
+    // instead of 22% at 256
+    const int Js[5] = {8, 7, 4, 2, 1};
     for (int J : Js) {
-        const double eff = scheme == S_2U ? (J == 8 ? 1.0 : J == 4 ? 1.06 : J == 2 ? 1.1 : 1.35)
+        if (J == 7 && scheme != S_2U) continue;
+        const double eff = scheme == S_2U ? (J == 8 ? 1.0 : J == 7 ? 1.02 : J == 4 ? 1.06 : J == 2 ? 1.1 : 1.35)
                                           : (J == 2 ? 1.0 : J == 4 ? 1.01 : J == 8 ? 1.02 : 1.02);
         for (int tpb = 32; tpb <= 256; tpb += 32) {
             const uint64_t jtile = (uint64_t)tpb * J;
