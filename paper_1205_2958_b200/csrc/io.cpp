@@ -325,7 +325,7 @@ private:
 // than parsing a small corpus takes.
 struct TextRes {
     int device = -1;  // -1: CPU parsing only (plain heap buffer)
-    TextBuf buf;
+    TextBuf buf, alt;  // alt: the device parser's second window (GPU mode only)
     std::unique_ptr<GpuLibsvmParser> gpu;
 };
 std::mutex g_text_mu;
@@ -352,6 +352,7 @@ std::unique_ptr<TextRes> lease_text_res(int device) {
         cudaGetLastError();
     }
     r->buf.set_pinned(r->gpu != nullptr);
+    r->alt.set_pinned(r->gpu != nullptr);
     return r;
 }
 
@@ -376,12 +377,26 @@ public:
         buf_ = &res_->buf;
         gpu_ = res_->gpu.get();
         gpu_block_ = gpu_parse_block_bytes(kGpuBlock);
-        // GPU mode: room for the block being parsed, the read-ahead block and
-        // several more, so the window slides before it has to be compacted
-        buf_->resize(gpu_ ? std::max(2 * kBlock, 8 * gpu_block_) + 1 : 2 * kBlock + 1);
+        // GPU mode: two windows, each with room for the block being parsed,
+        // the next one, the read-ahead block and a few more
+        // (a block size set through the test knob sizes the windows alone, so
+        // small corpora exercise the window switch)
+        const size_t win = gpu_block_ == kGpuBlock ? std::max(2 * kBlock, 6 * gpu_block_) : 6 * gpu_block_;
+        win_ = gpu_ ? win : 2 * kBlock;
+        buf_->resize(win_ + 1);
+        if (gpu_) {
+            alt_ = &res_->alt;
+            alt_->resize(win_ + 1);
+        }
     }
     ~LibsvmReader() override {
         if (f_) std::fclose(f_);
+        if (gpu_) {
+            try {
+                gpu_->cancel_prefetch();
+            } catch (...) {
+            }
+        }
         return_text_res(std::move(res_));
     }
 
@@ -417,104 +432,199 @@ private:
     static constexpr size_t kBlock = size_t(64) << 20;
     static constexpr size_t kGpuBlock = size_t(32) << 20;
 
-    // One block of complete lines through the GPU parser. Returns 1 if the
-    // block was consumed, 0 at the end of input, 2 if it does not fit the
-    // batch (it starts the next one), -1 if it must go through the CPU parser
-    // (set up via cpu_until_).
-    int gpu_block(Batch& b, uint64_t max_docs, uint64_t max_ids) {
-        const uint64_t rows_left = max_docs - b.n;
-        // size the block from the bytes per line / per id seen so far so its
-        // rows and ids fit the batch; when less than ~2 lines' worth is left,
-        // the batch is full and the block starts the next one
+    // Where a GPU block starting at `start` ends: 1 with [start, cut) set, 0 at
+    // the end of input, 2 if the batch is full, 3 if more input must be read
+    // first (only when !may_refill; refilling needs start == pos_). The block
+    // is sized from the bytes per line / per id seen so far to what the batch
+    // still takes, plus a little: the parser keeps the prefix that fits.
+    int plan_block(uint64_t rows_left, uint64_t ids_left, bool batch_empty, size_t start, size_t& cut,
+                   bool& at_eof, bool may_refill) {
         size_t target = gpu_block_;
         if (lines_seen_) {
             const double per_line = double(bytes_seen_) / double(lines_seen_);
             const double per_id = ids_seen_ ? double(bytes_seen_) / double(ids_seen_) : 4.0;
-            const uint64_t ids_left = max_ids > b.nids() ? max_ids - b.nids() : 0;
-            double fit = 0.9 * per_line * double(rows_left);
-            if (b.n > 0) fit = std::min(fit, 0.9 * per_id * double(ids_left));
-            if (b.n > 0 && fit < 2 * per_line) return 2;
+            double fit = per_line * double(rows_left);
+            if (!batch_empty) fit = std::min(fit, per_id * double(ids_left));
+            if (!batch_empty && fit < 0.5 * per_line) return 2;
+            fit = 1.05 * fit + 2 * per_line;
             if (fit < double(target)) target = std::max<size_t>(4096, size_t(fit));
         }
         for (;;) {
-            if (len_ - pos_ < target && !eof_) {
+            const bool final = sealed_ || eof_;  // the window's data ends at a line end / the file's end
+            if (len_ - start < target && !final) {
+                if (!may_refill) return 3;
                 trace("reader: refill");
                 refill();
                 trace("reader: refilled");
                 continue;
             }
-            if (pos_ >= len_) return 0;
-            const size_t end = std::min(len_, pos_ + target);
-            size_t cut = 0;
-            if (end == len_ && eof_) {
+            if (start >= len_) {
+                if (!sealed_) return 0;
+                if (!may_refill) return 3;
+                unseal();  // the window is drained: go on in the next one
+                continue;
+            }
+            const size_t end = std::min(len_, start + target);
+            cut = 0;
+            if (end == len_ && final) {
                 cut = len_;
             } else {
-                const void* nl = memrchr(buf_->data() + pos_, '\n', end - pos_);
+                const void* nl = memrchr(buf_->data() + start, '\n', end - start);
                 if (nl) cut = size_t(static_cast<const char*>(nl) - buf_->data()) + 1;
             }
             if (!cut) {  // one line longer than the block: widen it
-                if (eof_ && end == len_) return 0;
+                if (final && end == len_) return 0;
                 target *= 2;
                 continue;
             }
-            const bool at_eof = cut == len_ && eof_;
-            auto reserve = [&](uint64_t need) {
-                if (need > b.cap_ids) b.reserve_ids(need + (1u << 20));
-                return b.ids;
-            };
-            // read ahead into the free tail of the buffer while the GPU parses
-            // [pos_, cut): disjoint regions, joined before anything moves
-            std::thread ahead;
-            size_t ahead_got = 0;
-            std::exception_ptr ahead_err;
-            if (!eof_ && buf_->size() - 1 - len_ >= gpu_block_) {
-                ahead = std::thread([&] {
-                    try {
-                        ahead_got = read_at(buf_->data() + len_, gpu_block_);
-                    } catch (...) {
-                        ahead_err = std::current_exception();
-                    }
-                });
-            }
-            GpuParseResult r;
-            try {
-                r = gpu_->parse(buf_->data() + pos_, cut - pos_, at_eof, b.nids(), rows_left,
-                                b.n == 0 ? UINT64_MAX : max_ids - std::min(max_ids, b.nids()),
-                                reserve, b.row_ptr, b.labels);
-            } catch (...) {
-                if (ahead.joinable()) ahead.join();
-                throw;
-            }
-            if (ahead.joinable()) {
-                ahead.join();
-                if (ahead_err) std::rethrow_exception(ahead_err);
-                len_ += ahead_got;
-                if (ahead_got < gpu_block_) eof_ = true;
-            }
-            if (!r.ok) {
-                if (r.over_budget && b.n > 0) {
-                    trace("reader: batch full");
-                    return 2;  // this block starts the next batch
-                }
-                trace("reader: gpu block declined");
-                cpu_until_ = cut;
-                return -1;
-            }
-            if (trace_on()) {
-                char msg[96];
-                std::snprintf(msg, sizeof msg, "reader: gpu block parsed (%zu bytes, %llu rows)",
-                              size_t(cut - pos_), (unsigned long long)r.rows);
-                trace(msg);
-            }
-            b.n += r.rows;
-            line_no_ += r.lines;
-            lines_seen_ += r.lines;
-            bytes_seen_ += cut - pos_;
-            ids_seen_ += r.ids;
-            pos_ = cut;
-            gpu_blocks_ += 1;
-            return pos_ < len_ || !eof_ || r.rows ? 1 : 0;
+            at_eof = cut == len_ && eof_ && !sealed_;
+            return 1;
         }
+    }
+
+    // The current window is used up; its successor (holding the line the
+    // window's data stopped in the middle of, and what was read after it)
+    // becomes current.
+    void unseal() {
+        if (gpu_) gpu_->cancel_prefetch();  // the old window is about to be overwritten
+        std::swap(buf_, alt_);
+        buf_off_ = alt_off_;
+        len_ = alt_len_;
+        pos_ = 0;
+        cpu_until_ = 0;
+        alt_len_ = 0;
+        sealed_ = false;
+    }
+
+    uint64_t file_pos(size_t buf_pos) const { return buf_off_ + buf_pos; }
+
+    // One block of complete lines through the GPU parser. Returns 1 if the
+    // block was consumed, 0 at the end of input, 2 if the batch is full (the
+    // rest starts the next one), -1 if it must go through the CPU parser (set
+    // up via cpu_until_).
+    //
+    // While the GPU parses [pos_, cut), a host thread reads the next block
+    // into the free tail of the window. When the tail is full the window is
+    // sealed at its last line end: the partial line after it starts the other
+    // window, reading goes on there, and the GPU drains this one first. Blocks
+    // never straddle windows and only a partial line is ever copied. The copy
+    // of the block after this one to the device starts as soon as this
+    // block's kernels are queued.
+    int gpu_block(Batch& b, uint64_t max_docs, uint64_t max_ids) {
+        const uint64_t rows_left = max_docs - b.n;
+        const uint64_t ids_left = max_ids - std::min(max_ids, b.nids());
+        const bool empty = b.n == 0;
+        size_t cut = 0;
+        bool at_eof = false;
+        const int plan = plan_block(rows_left, ids_left, empty, pos_, cut, at_eof, true);
+        if (plan != 1) return plan;
+        const uint64_t key = file_pos(pos_);
+        // the next block as planned now (the batch state moves on, so it may
+        // be planned differently when it comes: that only wastes the copy)
+        size_t ncut = 0;
+        bool neof = false;
+        const bool next = cut < len_ && plan_block(rows_left, ids_left, empty, cut, ncut, neof, false) == 1;
+        const uint64_t nkey = file_pos(cut);
+
+        enum { kNone, kTail, kSeal, kAltTail } mode = kNone;
+        size_t seal_at = 0;
+        if (!eof_) {
+            if (!sealed_) {
+                if (win_ - len_ >= gpu_block_) {
+                    mode = kTail;
+                } else {
+                    // seal after the last line end (the blocks planned so far end before it)
+                    const void* nl = memrchr(buf_->data() + cut, '\n', len_ - cut);
+                    seal_at = nl ? size_t(static_cast<const char*>(nl) - buf_->data()) + 1 : cut;
+                    if (win_ >= len_ - seal_at + gpu_block_) mode = kSeal;
+                }
+            } else if (win_ - alt_len_ >= gpu_block_) {
+                mode = kAltTail;
+            }
+        }
+        std::thread ahead;
+        size_t ahead_got = 0;
+        std::exception_ptr ahead_err;
+        if (mode != kNone) {
+            ahead = std::thread([&] {
+                try {
+                    if (mode == kTail) {
+                        ahead_got = read_at(buf_->data() + len_, gpu_block_);
+                    } else if (mode == kSeal) {
+                        std::memcpy(alt_->data(), buf_->data() + seal_at, len_ - seal_at);
+                        ahead_got = read_at(alt_->data() + (len_ - seal_at), gpu_block_);
+                    } else {
+                        ahead_got = read_at(alt_->data() + alt_len_, gpu_block_);
+                    }
+                    trace("ahead: read");
+                } catch (...) {
+                    ahead_err = std::current_exception();
+                }
+            });
+        }
+        auto reserve = [&](uint64_t need) {
+            if (need > b.cap_ids) b.reserve_ids(need + (1u << 20));
+            return b.ids;
+        };
+        GpuParseResult r;
+        try {
+            r = gpu_->parse(buf_->data() + pos_, cut - pos_, at_eof, b.nids(), rows_left,
+                            empty ? UINT64_MAX : ids_left, reserve, b.row_ptr, b.labels, key,
+                            next ? buf_->data() + cut : nullptr, next ? ncut - cut : 0, nkey);
+        } catch (...) {
+            if (ahead.joinable()) ahead.join();
+            throw;
+        }
+        const bool whole = r.ok && r.bytes == cut - pos_;
+        if (ahead.joinable()) {
+            ahead.join();
+            if (ahead_err) std::rethrow_exception(ahead_err);
+            if (ahead_got < gpu_block_) eof_ = true;
+            if (mode == kTail) {
+                len_ += ahead_got;
+            } else if (mode == kSeal) {
+                alt_off_ = buf_off_ + seal_at;
+                alt_len_ = len_ - seal_at + ahead_got;
+                len_ = seal_at;
+                sealed_ = true;
+            } else {
+                alt_len_ += ahead_got;
+            }
+        }
+        if (!r.ok) {
+            if (r.over_budget && b.n > 0) {
+                trace("reader: batch full");
+                return 2;  // this block starts the next batch
+            }
+            trace("reader: gpu block declined");
+            cpu_until_ = cut;
+            return -1;
+        }
+        if (trace_on()) {
+            char msg[96];
+            std::snprintf(msg, sizeof msg, "reader: gpu block parsed (%zu bytes, %llu rows)",
+                          size_t(r.bytes), (unsigned long long)r.rows);
+            trace(msg);
+        }
+        b.n += r.rows;
+        line_no_ += r.lines;
+        lines_seen_ += r.lines;
+        bytes_seen_ += r.bytes;
+        ids_seen_ += r.ids;
+        pos_ += r.bytes;
+        gpu_blocks_ += 1;
+        if (sealed_ && pos_ == len_) unseal();  // so the next window's first block can be prefetched
+        // the next block's copy, if the one started above was planned otherwise
+        // (a full batch: the next one starts empty)
+        size_t cut2 = 0;
+        bool eof2 = false;
+        const bool full = !whole;
+        if (plan_block(full ? max_docs : max_docs - b.n, full ? max_ids : max_ids - std::min(max_ids, b.nids()),
+                       full || b.n == 0, pos_, cut2, eof2, false) == 1 &&
+            !gpu_->prefetched(file_pos(pos_), cut2 - pos_))
+            gpu_->prefetch(buf_->data() + pos_, cut2 - pos_, file_pos(pos_));
+        if (full) return 2;
+        return pos_ < len_ || sealed_ || !eof_ || r.rows ? 1 : 0;
     }
 
     // Finds the next line starting at pos_; reads more input as needed.
@@ -528,7 +638,7 @@ private:
                 pos_ = e + 1;
                 return true;
             }
-            if (eof_) {
+            if (eof_ && !sealed_) {
                 if (pos_ < len_) {  // last line without a newline
                     (*buf_)[len_] = '\0';
                     lines.emplace_back(pos_, len_);
@@ -543,18 +653,42 @@ private:
     }
 
     void refill() {
+        if (gpu_) gpu_->cancel_prefetch();  // its host bytes are about to move
+        if (sealed_) {
+            // (the window ends at a line end, so it is drained by now; keep any
+            // rest anyway, in front of the next window's data)
+            const size_t rest = len_ - pos_;
+            if (rest) {
+                if (alt_len_ + rest > win_) grow_windows(alt_len_ + rest);
+                std::memmove(alt_->data() + rest, alt_->data(), alt_len_);
+                std::memcpy(alt_->data(), buf_->data() + pos_, rest);
+                alt_off_ -= rest;
+                alt_len_ += rest;
+                pos_ = len_;
+            }
+            unseal();
+            return;
+        }
         if (pos_ > 0) {
             std::memmove(buf_->data(), buf_->data() + pos_, len_ - pos_);
             len_ -= pos_;
+            buf_off_ += pos_;
             cpu_until_ = cpu_until_ > pos_ ? cpu_until_ - pos_ : 0;
             pos_ = 0;
         }
-        if (len_ + kBlock / 2 > buf_->size() - 1) buf_->resize(std::max(buf_->size() * 2, len_ + kBlock + 1));
-        size_t want = buf_->size() - 1 - len_;
-        if (gpu_) want = std::min(want, std::max(gpu_block_, size_t(1) << 20));  // rest: read-ahead
+        const size_t room = gpu_ ? gpu_block_ : kBlock / 2;
+        if (len_ + room > win_) grow_windows(len_ + 2 * room);
+        size_t want = win_ - len_;
+        if (gpu_) want = std::min(want, std::max(2 * gpu_block_, size_t(1) << 20));  // rest: read-ahead
         const size_t got = read_at(buf_->data() + len_, want);
         if (got < want) eof_ = true;
         len_ += got;
+    }
+
+    void grow_windows(size_t need) {
+        win_ = std::max(win_ * 2, need);
+        buf_->resize(win_ + 1);
+        if (alt_) alt_->resize(win_ + 1);
     }
 
     void compact_if_needed() {}
@@ -667,6 +801,11 @@ private:
     FILE* f_ = nullptr;
     std::unique_ptr<TextRes> res_;  // pooled: pinned text buffer + device parser
     TextBuf* buf_ = nullptr;
+    TextBuf* alt_ = nullptr;  // GPU mode: the other window (see gpu_block)
+    size_t win_ = 0;          // window size in use (both buffers hold at least win_ + 1)
+    bool sealed_ = false;     // buf_ ends at len_; the data after it is in alt_ (see gpu_block)
+    size_t alt_len_ = 0;      // bytes in alt_ while sealed_
+    uint64_t buf_off_ = 0, alt_off_ = 0;  // file offsets of buf_[0], alt_[0]
     uint64_t file_off_ = 0;  // bytes of the file consumed by read_at
     size_t pos_ = 0, len_ = 0;
     bool eof_ = false;

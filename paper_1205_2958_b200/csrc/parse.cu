@@ -222,6 +222,25 @@ __global__ void row_emit(uint32_t nlines, const uint32_t* __restrict__ row_flag_
     if (li == nlines - 1) flags[1] = r + (row ? 1u : 0u);
 }
 
+// The longest prefix of whole lines within the budget when the whole block is
+// not: the line count L in [1, nlines) with L lines in budget and L + 1 not
+// (rows and ids before a line only grow). flags[4..8) = L, its rows, its ids,
+// its bytes; untouched (0) if not even one line fits.
+__global__ void prefix_cut(uint32_t nlines, const uint32_t* __restrict__ rows_before,
+                           const uint32_t* __restrict__ colons_before,
+                           const uint64_t* __restrict__ line_end, uint64_t max_rows,
+                           uint64_t max_ids, uint32_t* __restrict__ flags) {
+    const uint64_t L = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (L >= nlines) return;
+    auto fits = [&](uint64_t n) { return rows_before[n] <= max_rows && colons_before[n] <= max_ids; };
+    if (fits(L) && (L + 1 == nlines || !fits(L + 1))) {
+        flags[4] = uint32_t(L);
+        flags[5] = rows_before[L];
+        flags[6] = colons_before[L];
+        flags[7] = uint32_t(line_end[L - 1] + 1);
+    }
+}
+
 template <typename T>
 void grow_dev(T*& p, uint64_t& cap, uint64_t need) {
     if (need <= cap) return;
@@ -248,12 +267,18 @@ uint64_t gpu_parse_block_bytes(uint64_t dflt) {
 GpuLibsvmParser::GpuLibsvmParser(int device) : device_(device) {
     BBMH_CUDA(cudaSetDevice(device));
     BBMH_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-    BBMH_CUDA(cudaMalloc(&d_flags_, 4 * sizeof(uint32_t)));
-    BBMH_CUDA(cudaMallocHost(&h_flags_, 4 * sizeof(uint32_t)));
+    BBMH_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+    BBMH_CUDA(cudaEventCreateWithFlags(&copied_, cudaEventDisableTiming));
+    BBMH_CUDA(cudaMalloc(&d_flags_, 8 * sizeof(uint32_t)));
+    BBMH_CUDA(cudaMallocHost(&h_flags_, 8 * sizeof(uint32_t)));
 }
 
 GpuLibsvmParser::~GpuLibsvmParser() {
     cudaSetDevice(device_);
+    if (copy_st_) cudaStreamSynchronize(copy_st_);
+    if (d_next_) cudaFree(d_next_);
+    if (copied_) cudaEventDestroy(copied_);
+    if (copy_st_) cudaStreamDestroy(copy_st_);
     for (void* p : {(void*)d_text_, (void*)d_seg_, (void*)d_line_end_, (void*)d_colons_before_,
                     (void*)d_line_tok_, (void*)d_row_of_line_, (void*)d_line_label_, (void*)d_ids_,
                     (void*)d_row_end_, (void*)d_labels_, (void*)d_flags_, d_scan_tmp_})
@@ -263,24 +288,36 @@ GpuLibsvmParser::~GpuLibsvmParser() {
 }
 
 GpuParseResult GpuLibsvmParser::run(const char* text, uint64_t len, bool at_eof, uint64_t max_rows,
-                                    uint64_t max_ids) {
+                                    uint64_t max_ids, uint64_t key, const char* next_text,
+                                    uint64_t next_len, uint64_t next_key) {
     GpuParseResult r;
     if (len == 0 || len >= (1ull << 32)) return r;
     BBMH_CUDA(cudaSetDevice(device_));
     // 16 bytes of slack: the segment counter reads whole uint4 of full segments only
-    uint64_t cap_text = cap_text_;
-    grow_dev(d_text_, cap_text, len + 16);
-    cap_text_ = cap_text;
+    if (prefetched(key, len)) {
+        // the copy started by prefetch(): swap its buffer in, order after it
+        std::swap(d_text_, d_next_);
+        std::swap(cap_text_, cap_next_);
+        BBMH_CUDA(cudaStreamWaitEvent(st_, copied_, 0));
+        pf_len_ = 0;
+    } else {
+        cancel_prefetch();
+        uint64_t cap_text = cap_text_;
+        grow_dev(d_text_, cap_text, len + 16);
+        cap_text_ = cap_text;
+        BBMH_CUDA(cudaMemcpyAsync(d_text_, text, len, cudaMemcpyHostToDevice, st_));
+    }
     const uint64_t nchunk = (len + 15) / 16;
     const uint64_t nseg = (nchunk + kTpb - 1) / kTpb;  // CTAs
     uint64_t cap_seg = cap_seg_;
     grow_dev(d_seg_, cap_seg, nseg);
     cap_seg_ = cap_seg;
-    BBMH_CUDA(cudaMemcpyAsync(d_text_, text, len, cudaMemcpyHostToDevice, st_));
-    BBMH_CUDA(cudaMemsetAsync(d_flags_, 0, 4 * sizeof(uint32_t), st_));
+    BBMH_CUDA(cudaMemsetAsync(d_flags_, 0, 8 * sizeof(uint32_t), st_));
     const int tpb = 128;
     seg_count<<<unsigned(nseg), kTpb, 0, st_>>>(d_text_, len, d_seg_, d_flags_);
     BBMH_CUDA(cudaGetLastError());
+    // the next block's copy overlaps this block's kernels
+    if (next_len) prefetch(next_text, next_len, next_key);
     size_t tmp = 0;
     BBMH_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, d_seg_, d_seg_, int(nseg), st_));
     if (tmp > scan_tmp_bytes_) {
@@ -300,10 +337,6 @@ GpuParseResult GpuLibsvmParser::run(const char* text, uint64_t len, bool at_eof,
     const bool open_last = at_eof && text[len - 1] != '\n';
     const uint64_t nlines = nl + (open_last ? 1 : 0);
     if (nlines == 0) return r;
-    if (ncol > max_ids) {
-        r.over_budget = true;
-        return r;
-    }
     uint64_t cl = cap_lines_;
     grow_dev(d_line_end_, cl, nlines + 1);
     uint64_t cl2 = cap_lines_;
@@ -353,15 +386,59 @@ GpuParseResult GpuLibsvmParser::run(const char* text, uint64_t len, bool at_eof,
     trace("parse: checked");
     if (h_flags_[0] || h_flags_[2] != nlines || h_flags_[3] != ncol) return r;
     const uint64_t rows = h_flags_[1];
-    if (rows > max_rows) {
+    if (rows <= max_rows && ncol <= max_ids) {
+        r.ok = true;
+        r.lines = nlines;
+        r.rows = rows;
+        r.ids = ncol;
+        r.bytes = len;
+        return r;
+    }
+    // more than the batch takes: its longest prefix of whole lines that fits
+    prefix_cut<<<unsigned((nlines + tpb - 1) / tpb), tpb, 0, st_>>>(
+        uint32_t(nlines), d_row_of_line_, d_colons_before_, d_line_end_, max_rows, max_ids, d_flags_);
+    BBMH_CUDA(cudaGetLastError());
+    count_launches(1);
+    BBMH_CUDA(cudaMemcpyAsync(h_flags_ + 4, d_flags_ + 4, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+    BBMH_CUDA(cudaStreamSynchronize(st_));
+    if (!h_flags_[4]) {
         r.over_budget = true;
         return r;
     }
     r.ok = true;
-    r.lines = nlines;
-    r.rows = rows;
-    r.ids = ncol;
+    r.lines = h_flags_[4];
+    r.rows = h_flags_[5];
+    r.ids = h_flags_[6];
+    r.bytes = h_flags_[7];
     return r;
+}
+
+void GpuLibsvmParser::prefetch(const char* text, uint64_t len, uint64_t key) {
+    cancel_prefetch();
+    if (len == 0 || len >= (1ull << 32)) return;
+    BBMH_CUDA(cudaSetDevice(device_));
+    // the copy may only overwrite d_next_ once the parse that last used it as
+    // its text is done: every parse synchronises st_ before returning
+    uint64_t cap = cap_next_;
+    grow_dev(d_next_, cap, len + 16);
+    cap_next_ = cap;
+    BBMH_CUDA(cudaMemcpyAsync(d_next_, text, len, cudaMemcpyHostToDevice, copy_st_));
+    BBMH_CUDA(cudaEventRecord(copied_, copy_st_));
+    pf_key_ = key;
+    pf_len_ = len;
+    pf_waited_ = false;
+}
+
+void GpuLibsvmParser::wait_prefetch() {
+    if (!pf_len_ || pf_waited_) return;
+    BBMH_CUDA(cudaSetDevice(device_));
+    BBMH_CUDA(cudaEventSynchronize(copied_));
+    pf_waited_ = true;
+}
+
+void GpuLibsvmParser::cancel_prefetch() {
+    wait_prefetch();
+    pf_len_ = 0;
 }
 
 void GpuLibsvmParser::fetch(uint32_t* ids_out, uint64_t id_base, std::vector<uint64_t>& row_ptr,

@@ -25,6 +25,7 @@ struct GpuParseResult {
     uint64_t lines = 0;        // lines consumed (blank ones included)
     uint64_t rows = 0;         // non-blank lines
     uint64_t ids = 0;          // ids written
+    uint64_t bytes = 0;        // bytes consumed: the block, or the prefix that fit the budget
 };
 
 class GpuLibsvmParser {
@@ -38,21 +39,37 @@ public:
     // end of the file (`at_eof`). On success the rows are appended: ids (0-based)
     // to ids_out (capacity checked through `reserve`, which may move it),
     // row ends (offset by `id_base`) to row_ptr, labels to labels. At most
-    // max_rows rows and max_ids ids are accepted; a larger block is declined.
+    // max_rows rows and max_ids ids are taken: from a block holding more, the
+    // longest prefix of whole lines within both (r.bytes < len); if not even
+    // its first row fits, r.over_budget. `key` names the block (its file
+    // offset) for matching a prefetch; `next_*`, if set, is the block expected
+    // after this one, whose copy is started as soon as this one's kernels are
+    // queued.
     template <typename Reserve>
     GpuParseResult parse(const char* text, uint64_t len, bool at_eof, uint64_t id_base,
                          uint64_t max_rows, uint64_t max_ids, Reserve&& reserve,
-                         std::vector<uint64_t>& row_ptr, std::vector<int8_t>& labels) {
-        GpuParseResult r = run(text, len, at_eof, max_rows, max_ids);
+                         std::vector<uint64_t>& row_ptr, std::vector<int8_t>& labels,
+                         uint64_t key, const char* next_text = nullptr, uint64_t next_len = 0,
+                         uint64_t next_key = 0) {
+        GpuParseResult r = run(text, len, at_eof, max_rows, max_ids, key, next_text, next_len, next_key);
         if (!r.ok) return r;
         uint32_t* ids_out = reserve(id_base + r.ids);
         fetch(ids_out + id_base, id_base, row_ptr, labels, r);
         return r;
     }
 
+    // Starts the H2D copy of a block on a copy stream; parse() of the same
+    // (key, len) then skips its own copy. The host bytes must stay untouched
+    // until that parse() returns, wait_prefetch() or cancel_prefetch().
+    void prefetch(const char* text, uint64_t len, uint64_t key);
+    bool prefetched(uint64_t key, uint64_t len) const { return pf_len_ && pf_key_ == key && pf_len_ == len; }
+    void wait_prefetch();    // the pending copy's host bytes may be overwritten after this
+    void cancel_prefetch();  // wait_prefetch() and forget it
+
 private:
     GpuParseResult run(const char* text, uint64_t len, bool at_eof, uint64_t max_rows,
-                       uint64_t max_ids);
+                       uint64_t max_ids, uint64_t key, const char* next_text, uint64_t next_len,
+                       uint64_t next_key);
     void fetch(uint32_t* ids_out, uint64_t id_base, std::vector<uint64_t>& row_ptr,
                std::vector<int8_t>& labels, const GpuParseResult& r);
     void grow(uint64_t len);
@@ -60,7 +77,13 @@ private:
     int device_ = 0;
     cudaStream_t st_ = nullptr;
     uint64_t cap_text_ = 0, cap_seg_ = 0, cap_lines_ = 0, cap_ids_ = 0;
-    char* d_text_ = nullptr;
+    char* d_text_ = nullptr;     // text of the block being parsed
+    char* d_next_ = nullptr;     // prefetched text of the next block (swapped in)
+    uint64_t cap_next_ = 0;
+    cudaStream_t copy_st_ = nullptr;
+    cudaEvent_t copied_ = nullptr;
+    uint64_t pf_key_ = 0, pf_len_ = 0;  // the prefetched block (pf_len_ > 0: one is pending)
+    bool pf_waited_ = false;
     unsigned long long* d_seg_ = nullptr;   // per segment: newlines << 32 | colons, then scanned
     uint64_t* d_line_end_ = nullptr;        // position of each line's '\n' (or len)
     uint32_t* d_colons_before_ = nullptr;   // ids before each line start (lines + 1)
@@ -70,7 +93,7 @@ private:
     uint32_t* d_ids_ = nullptr;
     uint64_t* d_row_end_ = nullptr;         // rows: end (exclusive) in ids
     int8_t* d_labels_ = nullptr;
-    uint32_t* d_flags_ = nullptr;           // [0] bad, [1] rows
+    uint32_t* d_flags_ = nullptr;           // [0] bad, [1] rows, [2] lines, [3] ids, [4..8) prefix
     uint32_t* h_flags_ = nullptr;           // pinned mirror
     void* d_scan_tmp_ = nullptr;
     size_t scan_tmp_bytes_ = 0;
