@@ -105,3 +105,21 @@ def test_gpu_parse_errors_match_cpu(bb, ref, tmp_path, bad):
     for block in (None, 1 << 15):
         (g, _) = _sketch(bb, str(path), str(tmp_path / "gpu.bbmh"), gpu=True, block=block)
         assert g == cpu, (bad, block)
+
+
+def test_gpu_parse_lines_longer_than_the_window(bb, ref, tmp_path):
+    """Lines of ~50 KB against 4 KB blocks (24 KB windows): blocks widen past
+    the target, windows grow and seal around lines that do not fit them."""
+    rng = np.random.default_rng(5)
+    lines = _corpus(rng, 3000, False).split("\n")
+    for k in range(7, len(lines) - 1, 211):
+        ids = np.unique(rng.integers(0, 1 << 22, 6000)) + 1
+        lines[k] = "-1 " + " ".join("%d:1" % t for t in ids)
+    path = tmp_path / "long.txt"
+    path.write_text("\n".join(lines))  # no final newline
+    (cpu, _) = _sketch(bb, str(path), str(tmp_path / "cpu.bbmh"), gpu=False)
+    assert cpu[0] == 0, cpu
+    for block in (None, 4099, 1 << 15):
+        (g, launches) = _sketch(bb, str(path), str(tmp_path / "gpu.bbmh"), gpu=True, block=block)
+        assert g == cpu, block
+        assert launches > 4
