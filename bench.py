@@ -72,6 +72,27 @@ def make_corpus_device(torch, n, nnz, dim, seed, device):
     return row_ptr, idx
 
 
+def host_copy_gbps(bbmh, nbytes=1 << 30):
+    """Host DRAM bandwidth (read + write bytes/s) of a copy between two pinned
+    buffers split over all host cores (numpy releases the GIL while copying)."""
+    from concurrent.futures import ThreadPoolExecutor
+    T = os.cpu_count() or 1
+    src = bbmh.PinnedArray(nbytes, np.uint8)
+    dst = bbmh.PinnedArray(nbytes, np.uint8)
+    a, b = src.array, dst.array
+    a.fill(1)
+    cuts = [nbytes * w // T for w in range(T + 1)]
+    best = 0.0
+    with ThreadPoolExecutor(T) as ex:
+        for _ in range(4):
+            t = time.perf_counter()
+            list(ex.map(lambda w: np.copyto(b[cuts[w]:cuts[w + 1]], a[cuts[w]:cuts[w + 1]]), range(T)))
+            best = max(best, 2 * nbytes / (time.perf_counter() - t) / 1e9)
+    src.free()
+    dst.free()
+    return best
+
+
 def make_corpus_host(n, nnz, dim, seed):
     rng = np.random.default_rng(seed)
     u = np.sort(rng.random((n, nnz)), axis=1)
@@ -357,21 +378,29 @@ def run_ours(args):
         fam.sketch_csr(h_rp, pin.array, B, codes_out=codes_out.array)
     barrier()
     l0 = bbmh.kernel_launches()
+    x0 = bbmh.transfer_bytes()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         codes, _, flags = fam.sketch_csr(h_rp, pin.array, B, codes_out=codes_out.array)
     barrier()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
     e2e_launches = bbmh.kernel_launches() - l0
+    x1 = bbmh.transfer_bytes()
     # parity spot check of the e2e output against the device-resident run
     fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, B, d_codes.data_ptr(), None,
                           d_flags.data_ptr(), stream=stream.cuda_stream)
     torch.cuda.synchronize()
     e2e_consistent = bool(np.array_equal(d_codes[: 1000 * cb].cpu().numpy(),
                                          codes_out.array[: 1000 * cb]))
-    h2d = n * nnz * 4 + (n + 1) * 8
-    d2h = n * cb + n
-    # the e2e roofline for 2U is the PCIe H2D copy: measure pinned H2D bandwidth here
+    # bytes the library actually moved per step (ids go 2 B each as 16-bit row
+    # differences when the 4 B copy would bound the call: csrc/delta.hpp)
+    h2d = (x1[0] - x0[0]) // args.e2e_steps
+    d2h = (x1[1] - x0[1]) // args.e2e_steps
+    ids_bytes = n * nnz * 4
+    delta16 = h2d < ids_bytes
+    # host memory bandwidth: a pinned -> pinned copy on every host core (read + write)
+    host_best = host_copy_gbps(bbmh)
+    # the PCIe H2D copy bounds the 4-byte transfer: measure pinned H2D bandwidth here
     hb = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
     db = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
     db.copy_(hb, non_blocking=True)
@@ -438,10 +467,23 @@ def run_ours(args):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s * 1e3, "api": "bbmh_ext_sketch_csr (pinned host CSR)",
                     "consistent_with_device_run": e2e_consistent, "steps": args.e2e_steps,
-                    "roofline": {"bound": "pcie_h2d", "unit": "GB/s",
-                                 "achieved": h2d / e2e_s / 1e9, "peak": pcie_gbs,
-                                 "frac": h2d / e2e_s / 1e9 / pcie_gbs,
-                                 "peak_how": "pinned 1 GiB torch copy_ H2D, best of 3, this run"}},
+                    "transfer": ("ids as 16-bit row differences + escapes (csrc/delta.hpp), "
+                                 "rebuilt on the GPU" if delta16 else "ids as u32"),
+                    "input_GBps": ids_bytes / e2e_s / 1e9,
+                    "roofline": ({"bound": "host_memory", "unit": "GB/s",
+                                  "achieved": 8 * n * nnz / e2e_s / 1e9, "peak": host_best,
+                                  "frac": 8 * n * nnz / e2e_s / 1e9 / host_best,
+                                  "traffic_model": "8 B per id of host DRAM traffic: the encode "
+                                                   "reads 4 and writes 2, the DMA reads 2",
+                                  "peak_how": "1 GiB pinned -> pinned copy on all host cores "
+                                              "(read + write), best of 3, this run"}
+                                 if delta16 else
+                                 {"bound": "pcie_h2d", "unit": "GB/s",
+                                  "achieved": h2d / e2e_s / 1e9, "peak": pcie_gbs,
+                                  "frac": h2d / e2e_s / 1e9 / pcie_gbs,
+                                  "peak_how": "pinned 1 GiB torch copy_ H2D, best of 3, this run"}),
+                    "pcie_h2d": {"achieved": h2d / e2e_s / 1e9, "peak": pcie_gbs,
+                                 "frac": h2d / e2e_s / 1e9 / pcie_gbs}},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches_kernel + e2e_launches,

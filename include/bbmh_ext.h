@@ -101,6 +101,13 @@ BBMH_API void bbmh_ext_host_free(void* p);
  * (monotonic; used by benchmarks to report gpu_launches). */
 BBMH_API uint64_t bbmh_ext_kernel_launches(void);
 
+/* Bytes the host-buffer sketch paths (bbmh_ext_sketch_csr, bbmh_sketch_set
+ * batches, the file pipelines' chunks) have moved host->device and
+ * device->host in this process (monotonic). Ids may travel 2 bytes each
+ * (16-bit row differences, rebuilt on the device) where the copy would bound
+ * the call; these counts are the bytes actually moved. */
+BBMH_API void bbmh_ext_transfer_bytes(uint64_t* h2d_out, uint64_t* d2h_out);
+
 /* Chunk size (documents) used by the host-buffer and file pipelines;
  * 0 restores the default. */
 BBMH_API bbmh_status bbmh_ext_set_chunk_docs(uint64_t docs);

@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         "bbmh_ext_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], C.c_int32),
         "bbmh_ext_host_free": ([C.c_void_p], None),
         "bbmh_ext_kernel_launches": ([], C.c_uint64),
+        "bbmh_ext_transfer_bytes": ([u64p, u64p], None),
         "bbmh_ext_set_chunk_docs": ([C.c_uint64], C.c_int32),
     }
     for name, (args, res) in sig.items():
@@ -275,6 +276,13 @@ def set_chunk_docs(docs: int) -> None:
 
 def kernel_launches() -> int:
     return lib().bbmh_ext_kernel_launches()
+
+
+def transfer_bytes() -> tuple[int, int]:
+    """(host->device, device->host) bytes moved by the host-buffer sketch paths so far."""
+    a, b = C.c_uint64(0), C.c_uint64(0)
+    lib().bbmh_ext_transfer_bytes(C.byref(a), C.byref(b))
+    return a.value, b.value
 
 
 class PinnedArray:

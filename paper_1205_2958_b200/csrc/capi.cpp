@@ -294,6 +294,13 @@ void bbmh_ext_host_free(void* p) {
 
 uint64_t bbmh_ext_kernel_launches(void) { return kernel_launch_count(); }
 
+void bbmh_ext_transfer_bytes(uint64_t* h2d_out, uint64_t* d2h_out) {
+    uint64_t a = 0, b = 0;
+    transfer_counts(a, b);
+    if (h2d_out) *h2d_out = a;
+    if (d2h_out) *d2h_out = b;
+}
+
 bbmh_status bbmh_ext_set_chunk_docs(uint64_t docs) {
     return guarded([&] { set_chunk_docs(docs); });
 }

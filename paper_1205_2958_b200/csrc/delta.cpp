@@ -1,0 +1,139 @@
+// delta.cpp -- host side of the 2-byte id transfer encoding (see delta.hpp).
+// One pass over the ids: 8 per AVX2 step (two overlapping loads give each id
+// and its predecessor), escapes counted from the compare mask. Escaped values
+// are collected in a second pass over only the rows that have any.
+#include "delta.hpp"
+
+#include <immintrin.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "hostpool.hpp"
+
+namespace bbmh {
+
+namespace {
+
+// d in [1, 2^16) travels as is; 0 and >= 2^16 escape
+inline bool escapes(uint32_t d) { return d - 1u >= 65535u; }
+
+uint32_t encode_row_scalar(const uint32_t* s, uint16_t* o, uint64_t m, uint64_t i0, uint32_t prev) {
+    uint32_t c = 0;
+    for (uint64_t i = i0; i < m; ++i) {
+        const uint32_t d = s[i] - prev;
+        prev = s[i];
+        const bool e = escapes(d);
+        o[i] = e ? 0 : uint16_t(d);
+        c += e;
+    }
+    return c;
+}
+
+__attribute__((target("avx2"))) uint32_t encode_row_avx2(const uint32_t* s, uint16_t* o, uint64_t m) {
+    if (m == 0) return 0;
+    uint32_t c = escapes(s[0]);
+    o[0] = c ? 0 : uint16_t(s[0]);
+    uint64_t i = 1;
+    const __m256i hi = _mm256_set1_epi32(int(0xffff0000u));
+    const __m256i zero = _mm256_setzero_si256();
+    for (; i + 8 <= m; i += 8) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+        const __m256i p = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i - 1));
+        const __m256i d = _mm256_sub_epi32(a, p);
+        // escape: d has high bits, or d == 0
+        const __m256i small = _mm256_cmpeq_epi32(_mm256_and_si256(d, hi), zero);
+        const __m256i esc = _mm256_or_si256(_mm256_xor_si256(small, _mm256_set1_epi32(-1)),
+                                            _mm256_cmpeq_epi32(d, zero));
+        const __m256i v = _mm256_andnot_si256(esc, d);
+        const __m256i packed = _mm256_packus_epi32(v, v);  // per 128-bit lane: d0-3 d0-3 | d4-7 d4-7
+        _mm_storeu_si128(reinterpret_cast<__m128i*>(o + i),
+                         _mm256_castsi256_si128(_mm256_permute4x64_epi64(packed, 0x08)));
+        c += uint32_t(__builtin_popcount(unsigned(_mm256_movemask_ps(_mm256_castsi256_ps(esc)))));
+    }
+    return c + encode_row_scalar(s, o, m, i, s[i - 1]);
+}
+
+bool have_avx2() {
+    static const bool on = __builtin_cpu_supports("avx2");
+    return on;
+}
+
+}  // namespace
+
+bool delta16_worthwhile(const uint64_t* row_ptr, uint64_t n, uint64_t base, const uint32_t* ids) {
+    // sample up to 8 rows spread over the chunk: sorted, and a mean gap well
+    // under 2^16 (then escapes are rare: P(gap >= 2^16) ~ exp(-2^16 / mean))
+    uint64_t span = 0, cnt = 0;
+    const uint64_t step = std::max<uint64_t>(1, n / 8);
+    for (uint64_t r = 0; r < n; r += step) {
+        const uint64_t a = row_ptr[r] - base, b = row_ptr[r + 1] - base;
+        if (b - a < 2) continue;
+        const uint32_t* s = ids + a;
+        const uint64_t m = b - a;
+        for (uint64_t i = 1; i < std::min<uint64_t>(m, 64); ++i)
+            if (s[i] <= s[i - 1]) return false;
+        if (s[m - 1] <= s[0]) return false;
+        span += uint64_t(s[m - 1] - s[0]);
+        cnt += m - 1;
+    }
+    return cnt > 0 && span / cnt <= 8192;
+}
+
+bool encode_delta16(const uint64_t* row_ptr, uint64_t n, uint64_t base, const uint32_t* ids,
+                    uint16_t* deltas, uint32_t* exc_ptr, uint32_t* exc, uint64_t exc_cap,
+                    uint64_t& nexc) {
+    const uint64_t nidx = row_ptr[n] - base;
+    // tasks of >= 256 Ki ids, 4 per pool thread (taken dynamically: a thread
+    // the driver or the DMA interrupts holds nobody up), split at row
+    // boundaries by id count
+    const unsigned T = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(4 * host_threads(), nidx >> 18)));
+    std::vector<uint64_t> r0(T + 1);
+    for (unsigned w = 0; w <= T; ++w) {
+        const uint64_t target = base + nidx * w / T;
+        r0[w] = w == T ? n : uint64_t(std::lower_bound(row_ptr, row_ptr + n, target) - row_ptr);
+    }
+    std::vector<uint32_t> cnt(n);
+    std::vector<uint64_t> tot(T + 1, 0);
+    const bool avx2 = have_avx2();
+    host_parallel(T, [&](unsigned w) {
+        uint64_t t = 0;
+        for (uint64_t r = r0[w]; r < r0[w + 1]; ++r) {
+            const uint64_t a = row_ptr[r] - base, m = row_ptr[r + 1] - row_ptr[r];
+            const uint32_t c = avx2 ? encode_row_avx2(ids + a, deltas + a, m)
+                                    : encode_row_scalar(ids + a, deltas + a, m, 0, 0);
+            cnt[r] = c;
+            t += c;
+        }
+        tot[w + 1] = t;
+    });
+    for (unsigned w = 0; w < T; ++w) tot[w + 1] += tot[w];
+    nexc = tot[T];
+    if (nexc > exc_cap) return false;
+    // each task's escape offsets and values; escapes are rare where the
+    // encoding is used, so one serial pass unless there are many
+    auto place = [&](unsigned w) {
+        uint64_t at = tot[w];
+        for (uint64_t r = r0[w]; r < r0[w + 1]; ++r) {
+            exc_ptr[r] = uint32_t(at);
+            if (!cnt[r]) continue;
+            const uint32_t* s = ids + (row_ptr[r] - base);
+            const uint64_t m = row_ptr[r + 1] - row_ptr[r];
+            uint32_t prev = 0;
+            for (uint64_t i = 0; i < m; ++i) {
+                const uint32_t d = s[i] - prev;
+                prev = s[i];
+                if (escapes(d)) exc[at++] = d;
+            }
+        }
+    };
+    if (nexc > (1u << 16)) {
+        host_parallel(T, place);
+    } else {
+        for (unsigned w = 0; w < T; ++w) place(w);
+    }
+    exc_ptr[n] = uint32_t(nexc);
+    return true;
+}
+
+}  // namespace bbmh

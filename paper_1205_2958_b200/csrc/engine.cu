@@ -16,6 +16,8 @@
 #include <thread>
 
 #include "engine.hpp"
+#include "delta.hpp"
+#include "hostpool.hpp"
 
 namespace bbmh {
 
@@ -417,6 +419,16 @@ void Lane::reserve(Slot& s, uint64_t rows, uint64_t nidx, bool need_pinned_idx) 
 
 namespace {
 constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// the lanes' host<->device copies, counted (bbmh_ext_transfer_bytes)
+void h2d(void* d, const void* h, size_t n, cudaStream_t st) {
+    BBMH_CUDA(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, st));
+    count_transfer(n, 0);
+}
+void d2h(void* h, const void* d, size_t n, cudaStream_t st) {
+    BBMH_CUDA(cudaMemcpyAsync(h, d, n, cudaMemcpyDeviceToHost, st));
+    count_transfer(0, n);
+}
 }  // namespace
 
 // Chunks without minima: everything small the chunk moves goes through one
@@ -425,17 +437,47 @@ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 // small-batch case is bound by these API calls, not by bytes).
 //   H2D  [0, off_err+16):        row_ptr | ids (pageable input only) | err=0, bad=~0
 //   D2H  [off_err, blk_end):     err, bad | scores | flags | codes
+// When the ids' H2D would bound the chunk they go 2 bytes each instead
+// (delta.hpp), from pinned or pageable input alike:
+//   H2D  [0, off_err+16):        row_ptr | exc_ptr | u16 deltas | escapes | err, bad
+// and decode_delta16 rebuilds them in the slot's id buffer before the sketch.
+namespace {
+
+// BBMH_DELTA_H2D: 0 off, 1 on whenever possible (tests), unset: where it pays
+int delta16_mode() {
+    const char* e = std::getenv("BBMH_DELTA_H2D");  // read per chunk: tests flip it
+    return e && *e ? (*e == '0' ? 0 : 1) : 2;
+}
+
+// The H2D of 4 B per id bounds the chunk when the kernel's time per id is
+// below the copy's: 2U up to k ~ 1,000, 4U only at tiny k (kernel rates:
+// 14.5 T and 1.3 T evals/s against ~55 GB/s of PCIe, profiles/r10).
+bool delta16_pays(const KernelFamily& kf) {
+    if (kf.scheme == int32_t(Scheme::TwoU)) return kf.k <= 1024;
+    if (kf.scheme == int32_t(Scheme::Permutation)) return false;
+    return kf.k <= 64;
+}
+
+constexpr uint64_t kDeltaMinIds = 1ull << 16;
+
+}  // namespace
+
 void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     const uint64_t n = job.n;
+    const int dmode = delta16_mode();
+    bool delta = dmode != 0 && nidx > 0 &&
+                 (dmode == 1 || (nidx >= kDeltaMinIds && delta16_pays(df_->kf) &&
+                                 delta16_worthwhile(job.row_ptr, n, job.index_base, job.indices)));
     const bool inline_ids = !job.pinned_input;
-    s.off_ids = align16((n + 1) * sizeof(uint64_t));
-    s.off_err = align16(s.off_ids + (inline_ids ? nidx * sizeof(uint32_t) : 0));
-    s.off_scores = s.off_err + 16;
-    s.off_flags = s.off_scores + (d_w_ ? n * sizeof(double) : 0);
-    s.off_codes = s.off_flags + n;  // no gap: every byte copied back is written by a kernel
-    s.blk_end = s.off_codes + n * cb_;
-    if (s.blk_end > s.cap_blk) {
-        const uint64_t cap = std::max<uint64_t>(s.blk_end, s.cap_blk + s.cap_blk / 2);
+    const size_t raw_err = align16(align16((n + 1) * sizeof(uint64_t)) + (inline_ids ? nidx * sizeof(uint32_t) : 0));
+    const size_t d_exc_ptr = align16((n + 1) * sizeof(uint64_t));
+    const size_t d_deltas = align16(d_exc_ptr + (n + 1) * sizeof(uint32_t));
+    const size_t d_exc = align16(d_deltas + nidx * sizeof(uint16_t));
+    const uint64_t exc_cap = nidx / 8 + 64;
+    const size_t tail = 16 + (d_w_ ? n * sizeof(double) : 0) + n + n * cb_;
+    const size_t need = std::max(raw_err, delta ? align16(d_exc + exc_cap * sizeof(uint32_t)) : 0) + tail;
+    if (need > s.cap_blk) {
+        const uint64_t cap = std::max<uint64_t>(need, s.cap_blk + s.cap_blk / 2);
         if (s.d_blk) BBMH_CUDA(cudaFree(s.d_blk));
         if (s.h_blk) BBMH_CUDA(cudaFreeHost(s.h_blk));
         s.d_blk = nullptr;
@@ -446,23 +488,53 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     }
     s.packed = true;
     uint8_t* h = s.h_blk;
+    uint8_t* d = s.d_blk;
+    uint64_t nexc = 0;
+    if (delta)
+        delta = encode_delta16(job.row_ptr, n, job.index_base, job.indices,
+                               reinterpret_cast<uint16_t*>(h + d_deltas),
+                               reinterpret_cast<uint32_t*>(h + d_exc_ptr),
+                               reinterpret_cast<uint32_t*>(h + d_exc), exc_cap, nexc);
+    if (delta) trace("lane: ids encoded");
+    s.off_ids = delta ? d_deltas : align16((n + 1) * sizeof(uint64_t));
+    s.off_err = delta ? align16(d_exc + nexc * sizeof(uint32_t)) : raw_err;
+    s.off_scores = s.off_err + 16;
+    s.off_flags = s.off_scores + (d_w_ ? n * sizeof(double) : 0);
+    s.off_codes = s.off_flags + n;  // no gap: every byte copied back is written by a kernel
+    s.blk_end = s.off_codes + n * cb_;
     std::memcpy(h, job.row_ptr, (n + 1) * sizeof(uint64_t));
     // zero the alignment gaps too: every byte of the H2D block is defined
-    std::memset(h + (n + 1) * sizeof(uint64_t), 0, s.off_ids - (n + 1) * sizeof(uint64_t));
-    const size_t ids_end = s.off_ids + (inline_ids ? nidx * sizeof(uint32_t) : 0);
-    std::memset(h + ids_end, 0, s.off_err - ids_end);
-    if (inline_ids && nidx) std::memcpy(h + s.off_ids, job.indices, nidx * sizeof(uint32_t));
+    auto zero_gap = [&](size_t from, size_t to) {
+        if (to > from) std::memset(h + from, 0, to - from);
+    };
+    if (delta) {
+        zero_gap((n + 1) * sizeof(uint64_t), d_exc_ptr);
+        zero_gap(d_exc_ptr + (n + 1) * sizeof(uint32_t), d_deltas);
+        zero_gap(d_deltas + nidx * sizeof(uint16_t), d_exc);
+        zero_gap(d_exc + nexc * sizeof(uint32_t), s.off_err);
+    } else {
+        zero_gap((n + 1) * sizeof(uint64_t), s.off_ids);
+        const size_t ids_end = s.off_ids + (inline_ids ? nidx * sizeof(uint32_t) : 0);
+        zero_gap(ids_end, s.off_err);
+        if (inline_ids && nidx) host_memcpy(h + s.off_ids, job.indices, nidx * sizeof(uint32_t));
+    }
     std::memset(h + s.off_err, 0, 8);
     std::memset(h + s.off_err + 8, 0xff, 8);
-    uint8_t* d = s.d_blk;
     const uint32_t* d_ids = reinterpret_cast<const uint32_t*>(d + s.off_ids);
-    if (!inline_ids && nidx) {
+    if (delta || (!inline_ids && nidx)) {
         grow_device(s.d_idx, s.cap_idx, nidx + kIdsSlack);
-        BBMH_CUDA(cudaMemcpyAsync(s.d_idx, job.indices, nidx * sizeof(uint32_t),
-                                  cudaMemcpyHostToDevice, s.st));
         d_ids = s.d_idx;
     }
-    BBMH_CUDA(cudaMemcpyAsync(s.d_blk, h, s.off_err + 16, cudaMemcpyHostToDevice, s.st));
+    if (!delta && !inline_ids && nidx)
+        h2d(s.d_idx, job.indices, nidx * sizeof(uint32_t), s.st);
+    h2d(s.d_blk, h, s.off_err + 16, s.st);
+    if (delta) {
+        launch_decode_delta16(reinterpret_cast<const uint64_t*>(d), job.index_base, n,
+                              reinterpret_cast<const uint16_t*>(d + d_deltas),
+                              reinterpret_cast<const uint32_t*>(d + d_exc_ptr),
+                              reinterpret_cast<const uint32_t*>(d + d_exc), s.d_idx, s.st);
+        BBMH_CUDA(cudaGetLastError());
+    }
     auto* d_err = reinterpret_cast<int*>(d + s.off_err);
     auto* d_bad = reinterpret_cast<unsigned long long*>(d + s.off_err + 8);
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
@@ -476,8 +548,7 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
         BBMH_CUDA(cudaGetLastError());
     }
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
-    BBMH_CUDA(cudaMemcpyAsync(h + s.off_err, d + s.off_err, s.blk_end - s.off_err,
-                              cudaMemcpyDeviceToHost, s.st));
+    d2h(h + s.off_err, d + s.off_err, s.blk_end - s.off_err, s.st);
     BBMH_CUDA(cudaEventRecord(s.done, s.st));
     s.busy = true;
 }
@@ -497,16 +568,14 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
     reserve(s, n, nidx, stage);
     // row_ptr always goes through the slot's pinned mirror (small)
     std::memcpy(s.h_rp, job.row_ptr, (n + 1) * sizeof(uint64_t));
-    BBMH_CUDA(cudaMemcpyAsync(s.d_rp, s.h_rp, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                              s.st));
+    h2d(s.d_rp, s.h_rp, (n + 1) * sizeof(uint64_t), s.st);
     const uint32_t* src = job.indices;
     if (stage && nidx) {
-        std::memcpy(s.h_idx, job.indices, nidx * sizeof(uint32_t));
+        host_memcpy(s.h_idx, job.indices, nidx * sizeof(uint32_t));
         src = s.h_idx;
     }
     if (nidx)
-        BBMH_CUDA(cudaMemcpyAsync(s.d_idx, src, nidx * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                                  s.st));
+        h2d(s.d_idx, src, nidx * sizeof(uint32_t), s.st);
     BBMH_CUDA(cudaMemsetAsync(s.d_err, 0, sizeof(int), s.st));
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
     launch_sketch(df_->kf, s.d_rp, job.index_base, s.d_idx, n, b_, s.d_codes,
@@ -516,19 +585,16 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
         BBMH_CUDA(cudaMemsetAsync(s.d_bad, 0xff, sizeof(unsigned long long), s.st));
         launch_score(s.d_codes, s.d_flags, n, f_.k, b_, d_w_, wdim_, s.d_scores, s.d_bad, s.st);
         BBMH_CUDA(cudaGetLastError());
-        BBMH_CUDA(cudaMemcpyAsync(s.h_scores, s.d_scores, n * sizeof(double),
-                                  cudaMemcpyDeviceToHost, s.st));
-        BBMH_CUDA(cudaMemcpyAsync(s.h_bad, s.d_bad, sizeof(unsigned long long),
-                                  cudaMemcpyDeviceToHost, s.st));
+        d2h(s.h_scores, s.d_scores, n * sizeof(double), s.st);
+        d2h(s.h_bad, s.d_bad, sizeof(unsigned long long), s.st);
     }
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
     if (n && cb_)
-        BBMH_CUDA(cudaMemcpyAsync(s.h_codes, s.d_codes, n * cb_, cudaMemcpyDeviceToHost, s.st));
+        d2h(s.h_codes, s.d_codes, n * cb_, s.st);
     if (want_minima_)
-        BBMH_CUDA(cudaMemcpyAsync(s.h_min, s.d_min, n * f_.k * sizeof(uint64_t),
-                                  cudaMemcpyDeviceToHost, s.st));
-    BBMH_CUDA(cudaMemcpyAsync(s.h_flags, s.d_flags, n, cudaMemcpyDeviceToHost, s.st));
-    BBMH_CUDA(cudaMemcpyAsync(s.h_err, s.d_err, sizeof(int), cudaMemcpyDeviceToHost, s.st));
+        d2h(s.h_min, s.d_min, n * f_.k * sizeof(uint64_t), s.st);
+    d2h(s.h_flags, s.d_flags, n, s.st);
+    d2h(s.h_err, s.d_err, sizeof(int), s.st);
     BBMH_CUDA(cudaEventRecord(s.done, s.st));
     s.busy = true;
 }
@@ -640,6 +706,7 @@ bool sketch_rows_zero_copy(const Family& f, int dev, const uint64_t* row_ptr,
                   h + off_flags, s->d_err, s->st);
     BBMH_CUDA(cudaGetLastError());
     BBMH_CUDA(cudaStreamSynchronize(s->st));
+    count_transfer((n + 1) * sizeof(uint64_t) + (row_ptr[n] - row_ptr[0]) * sizeof(uint32_t), n + n * cb);
     if (codes) std::memcpy(codes, h + off_codes, n * cb);
     if (flags) std::memcpy(flags, h + off_flags, n);
     return true;
@@ -698,9 +765,9 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
             lane.set_timed(false);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
-                if (codes) std::memcpy(codes + r0 * cb, res.codes, res.n * cb);
+                if (codes) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);
                 if (scores) std::memcpy(scores + r0, res.scores, res.n * sizeof(double));
-                if (minima) std::memcpy(minima + r0 * f.k, res.minima, res.n * f.k * 8);
+                if (minima) host_memcpy(minima + r0 * f.k, res.minima, res.n * f.k * 8);
                 if (flags) std::memcpy(flags + r0, res.flags, res.n);
             };
             for (uint64_t c; !abort.load() && (c = next.fetch_add(1)) < nchunks;) {

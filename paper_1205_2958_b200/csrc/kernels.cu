@@ -720,4 +720,18 @@ uint64_t kernel_launch_count() { return g_launches.load(); }
 
 void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+namespace {
+std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+}  // namespace
+
+void count_transfer(uint64_t h2d, uint64_t d2h) {
+    g_h2d.fetch_add(h2d, std::memory_order_relaxed);
+    g_d2h.fetch_add(d2h, std::memory_order_relaxed);
+}
+
+void transfer_counts(uint64_t& h2d, uint64_t& d2h) {
+    h2d = g_h2d.load();
+    d2h = g_d2h.load();
+}
+
 }  // namespace bbmh

@@ -62,4 +62,9 @@ void launch_score(const uint8_t* codes, const uint8_t* flags, uint64_t n, uint32
 uint64_t kernel_launch_count();
 void count_launches(uint64_t n);
 
+// Bytes the host-buffer sketch paths move between host and device (copies,
+// and the zero-copy path's reads and writes of mapped host memory).
+void count_transfer(uint64_t h2d, uint64_t d2h);
+void transfer_counts(uint64_t& h2d, uint64_t& d2h);
+
 }  // namespace bbmh
