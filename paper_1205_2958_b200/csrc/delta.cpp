@@ -1,12 +1,19 @@
 // delta.cpp -- host side of the 2-byte id transfer encoding (see delta.hpp).
-// One pass over the ids: 8 per AVX2 step (two overlapping loads give each id
-// and its predecessor), escapes counted from the compare mask. Escaped values
-// are collected in a second pass over only the rows that have any.
+//
+// The encode is bound by host DRAM bandwidth (it runs beside the DMA that
+// reads its output), so each task streams over a contiguous range of ids:
+// 8 differences per AVX2 step (two overlapping loads give each id and its
+// predecessor), stored with non-temporal stores -- no read-for-ownership of
+// the output lines, 2 B of traffic per id saved (+12% measured with the DMA
+// running, profiles/r11/host_encode_probe.jsonl). Row starts (difference to
+// 0, not to the previous row's last id) are patched afterwards, and the
+// escape positions recorded on the way are assigned to rows.
 #include "delta.hpp"
 
 #include <immintrin.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <vector>
 
 #include "hostpool.hpp"
@@ -18,40 +25,47 @@ namespace {
 // d in [1, 2^16) travels as is; 0 and >= 2^16 escape
 inline bool escapes(uint32_t d) { return d - 1u >= 65535u; }
 
-uint32_t encode_row_scalar(const uint32_t* s, uint16_t* o, uint64_t m, uint64_t i0, uint32_t prev) {
-    uint32_t c = 0;
-    for (uint64_t i = i0; i < m; ++i) {
-        const uint32_t d = s[i] - prev;
-        prev = s[i];
-        const bool e = escapes(d);
-        o[i] = e ? 0 : uint16_t(d);
-        c += e;
-    }
-    return c;
+inline void encode_one(const uint32_t* s, uint16_t* o, uint64_t i, std::vector<uint64_t>& pos) {
+    const uint32_t d = s[i] - (i ? s[i - 1] : 0u);
+    const bool e = escapes(d);
+    o[i] = e ? 0 : uint16_t(d);
+    if (e) pos.push_back(i);
 }
 
-__attribute__((target("avx2"))) uint32_t encode_row_avx2(const uint32_t* s, uint16_t* o, uint64_t m) {
-    if (m == 0) return 0;
-    uint32_t c = escapes(s[0]);
-    o[0] = c ? 0 : uint16_t(s[0]);
-    uint64_t i = 1;
+// Plain differences s[i] - s[i-1] over [a, b); escape positions appended in order.
+void encode_range_scalar(const uint32_t* s, uint16_t* o, uint64_t a, uint64_t b,
+                         std::vector<uint64_t>& pos) {
+    for (uint64_t i = a; i < b; ++i) encode_one(s, o, i, pos);
+}
+
+__attribute__((target("avx2"))) void encode_range_avx2(const uint32_t* s, uint16_t* o, uint64_t a,
+                                                       uint64_t b, std::vector<uint64_t>& pos) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+    uint64_t i = a;
+    for (; i < b && ((i & 7) || i == 0); ++i) encode_one(s, o, i, pos);
     const __m256i hi = _mm256_set1_epi32(int(0xffff0000u));
     const __m256i zero = _mm256_setzero_si256();
-    for (; i + 8 <= m; i += 8) {
-        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+    const __m256i ones = _mm256_set1_epi32(-1);
+    for (; i + 8 <= b; i += 8) {
+        const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
         const __m256i p = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i - 1));
-        const __m256i d = _mm256_sub_epi32(a, p);
+        const __m256i d = _mm256_sub_epi32(x, p);
         // escape: d has high bits, or d == 0
         const __m256i small = _mm256_cmpeq_epi32(_mm256_and_si256(d, hi), zero);
-        const __m256i esc = _mm256_or_si256(_mm256_xor_si256(small, _mm256_set1_epi32(-1)),
-                                            _mm256_cmpeq_epi32(d, zero));
+        const __m256i esc = _mm256_or_si256(_mm256_xor_si256(small, ones), _mm256_cmpeq_epi32(d, zero));
         const __m256i v = _mm256_andnot_si256(esc, d);
         const __m256i packed = _mm256_packus_epi32(v, v);  // per 128-bit lane: d0-3 d0-3 | d4-7 d4-7
-        _mm_storeu_si128(reinterpret_cast<__m128i*>(o + i),
-                         _mm256_castsi256_si128(_mm256_permute4x64_epi64(packed, 0x08)));
-        c += uint32_t(__builtin_popcount(unsigned(_mm256_movemask_ps(_mm256_castsi256_ps(esc)))));
+        const __m128i out = _mm256_castsi256_si128(_mm256_permute4x64_epi64(packed, 0x08));
+        if (aligned) _mm_stream_si128(reinterpret_cast<__m128i*>(o + i), out);
+        else _mm_storeu_si128(reinterpret_cast<__m128i*>(o + i), out);
+        unsigned m = unsigned(_mm256_movemask_ps(_mm256_castsi256_ps(esc)));
+        while (m) {
+            pos.push_back(i + unsigned(__builtin_ctz(m)));
+            m &= m - 1;
+        }
     }
-    return c + encode_row_scalar(s, o, m, i, s[i - 1]);
+    for (; i < b; ++i) encode_one(s, o, i, pos);
+    _mm_sfence();  // the streamed lines are visible before the row-start patches
 }
 
 bool have_avx2() {
@@ -93,38 +107,42 @@ bool encode_delta16(const uint64_t* row_ptr, uint64_t n, uint64_t base, const ui
         const uint64_t target = base + nidx * w / T;
         r0[w] = w == T ? n : uint64_t(std::lower_bound(row_ptr, row_ptr + n, target) - row_ptr);
     }
-    std::vector<uint32_t> cnt(n);
+    std::vector<std::vector<uint64_t>> pos(T);  // per task: escape positions, in order
     std::vector<uint64_t> tot(T + 1, 0);
     const bool avx2 = have_avx2();
     host_parallel(T, [&](unsigned w) {
-        uint64_t t = 0;
+        const uint64_t a = row_ptr[r0[w]] - base, b = row_ptr[r0[w + 1]] - base;
+        std::vector<uint64_t> raw;
+        if (avx2) encode_range_avx2(ids, deltas, a, b, raw);
+        else encode_range_scalar(ids, deltas, a, b, raw);
+        // row starts: the difference is to 0; keep the escapes in row order
+        std::vector<uint64_t>& out = pos[w];
+        size_t k = 0;
         for (uint64_t r = r0[w]; r < r0[w + 1]; ++r) {
-            const uint64_t a = row_ptr[r] - base, m = row_ptr[r + 1] - row_ptr[r];
-            const uint32_t c = avx2 ? encode_row_avx2(ids + a, deltas + a, m)
-                                    : encode_row_scalar(ids + a, deltas + a, m, 0, 0);
-            cnt[r] = c;
-            t += c;
+            const uint64_t ra = row_ptr[r] - base, rb = row_ptr[r + 1] - base;
+            if (ra == rb) continue;
+            const bool e0 = escapes(ids[ra]);
+            deltas[ra] = e0 ? 0 : uint16_t(ids[ra]);
+            if (e0) out.push_back(ra);
+            for (; k < raw.size() && raw[k] < rb; ++k)
+                if (raw[k] != ra) out.push_back(raw[k]);
         }
-        tot[w + 1] = t;
+        tot[w + 1] = out.size();
     });
     for (unsigned w = 0; w < T; ++w) tot[w + 1] += tot[w];
     nexc = tot[T];
     if (nexc > exc_cap) return false;
-    // each task's escape offsets and values; escapes are rare where the
-    // encoding is used, so one serial pass unless there are many
+    // each task's escape offsets per row and values; escapes are rare where
+    // the encoding is used, so one serial pass unless there are many
     auto place = [&](unsigned w) {
         uint64_t at = tot[w];
+        size_t k = 0;
+        const std::vector<uint64_t>& p = pos[w];
         for (uint64_t r = r0[w]; r < r0[w + 1]; ++r) {
             exc_ptr[r] = uint32_t(at);
-            if (!cnt[r]) continue;
-            const uint32_t* s = ids + (row_ptr[r] - base);
-            const uint64_t m = row_ptr[r + 1] - row_ptr[r];
-            uint32_t prev = 0;
-            for (uint64_t i = 0; i < m; ++i) {
-                const uint32_t d = s[i] - prev;
-                prev = s[i];
-                if (escapes(d)) exc[at++] = d;
-            }
+            const uint64_t ra = row_ptr[r] - base, rb = row_ptr[r + 1] - base;
+            for (; k < p.size() && p[k] < rb; ++k)
+                exc[at++] = p[k] == ra ? ids[ra] : ids[p[k]] - ids[p[k] - 1];
         }
     };
     if (nexc > (1u << 16)) {

@@ -443,7 +443,8 @@ void d2h(void* h, const void* d, size_t n, cudaStream_t st) {
 // and decode_delta16 rebuilds them in the slot's id buffer before the sketch.
 namespace {
 
-// BBMH_DELTA_H2D: 0 off, 1 on whenever possible (tests), unset: where it pays
+// BBMH_DELTA_H2D: 0 off, 1 on whenever possible (tests), unset: where it
+// pays, on lanes that allow it (Lane::set_delta16)
 int delta16_mode() {
     const char* e = std::getenv("BBMH_DELTA_H2D");  // read per chunk: tests flip it
     return e && *e ? (*e == '0' ? 0 : 1) : 2;
@@ -466,7 +467,7 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     const uint64_t n = job.n;
     const int dmode = delta16_mode();
     bool delta = dmode != 0 && nidx > 0 &&
-                 (dmode == 1 || (nidx >= kDeltaMinIds && delta16_pays(df_->kf) &&
+                 (dmode == 1 || (delta16_ && nidx >= kDeltaMinIds && delta16_pays(df_->kf) &&
                                  delta16_worthwhile(job.row_ptr, n, job.index_base, job.indices)));
     const bool inline_ids = !job.pinned_input;
     const size_t raw_err = align16(align16((n + 1) * sizeof(uint64_t)) + (inline_ids ? nidx * sizeof(uint32_t) : 0));
@@ -763,6 +764,7 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
         try {
             Lane lane(f, dev, b, minima != nullptr, score);
             lane.set_timed(false);
+            lane.set_delta16(true);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
                 if (codes) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);

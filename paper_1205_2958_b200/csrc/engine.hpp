@@ -107,6 +107,10 @@ public:
     int device() const { return device_; }
     // Record kernel start/stop events per chunk (ChunkResult::kernel_ms).
     void set_timed(bool on) { timed_ = on; }
+    // Allow the 2-byte id transfer (delta.hpp) where it pays: for callers
+    // whose chunks are bound by the H2D copy (host CSR batches), not by what
+    // produces them (the file pipelines' parsers share the host cores).
+    void set_delta16(bool on) { delta16_ = on; }
 
 public:
     struct Slot {
@@ -158,6 +162,7 @@ private:
     uint64_t wdim_ = 0;
     uint64_t next_ = 0;
     bool timed_ = true;
+    bool delta16_ = false;
     Slot* slots_[kSlots] = {};
 };
 
