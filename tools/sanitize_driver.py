@@ -3,7 +3,7 @@
 power-of-two and general D, 4U-mod, permutation in both schedules, k
 spanning several CTAs, rows longer than one shared-memory tile, empty rows),
 the file pipeline on BBCV and on LibSVM text (GPU parser + CPU fallback),
-expansion to BBCV and LibSVM text, fused scoring,
+the 2-byte id transfer, expansion to BBCV and LibSVM text, fused scoring,
 predict on a BBMH file, all-pairs match counts and the VW projection.
 No torch; ctypes only. Usage: compute-sanitizer --tool memcheck python
 tools/sanitize_driver.py"""
@@ -33,6 +33,13 @@ def main():
             f.sketch_csr(long_rp, long_idx, 5)
             f.sketch_set(idx[: int(rp[1])], 3)
             f.sketch_score_csr(rp, idx, 4, rng.standard_normal(k << 4))
+    # ids through the 2-byte transfer (delta.cu): escapes, empty rows, a long row
+    os.environ["BBMH_DELTA_H2D"] = "1"
+    with bbmh.Family(1, 1 << 20, 70, 42) as f:
+        f.sketch_csr(rp, idx, 8)
+        f.sketch_csr(long_rp, long_idx, 8)
+        f.sketch_csr(rp, np.ascontiguousarray(idx[::-1]), 8)
+    os.environ.pop("BBMH_DELTA_H2D")
     os.environ["BBMH_PERM_TABLEWISE"] = "1"
     with bbmh.Family(0, 1 << 12, 9, 42) as f:
         f.sketch_csr(rp, idx % (1 << 12), 6, want_minima=True)
