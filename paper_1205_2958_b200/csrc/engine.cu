@@ -764,7 +764,10 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
         try {
             Lane lane(f, dev, b, minima != nullptr, score);
             lane.set_timed(false);
-            lane.set_delta16(true);
+            // one lane: the host cores are free to encode. Several lanes would
+            // share them, and N PCIe links reading 4 B per id beat one host
+            // encoding at 8 B of DRAM traffic per id.
+            lane.set_delta16(devs.size() == 1);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
                 if (codes) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);
