@@ -461,6 +461,13 @@ bool delta16_pays(const KernelFamily& kf) {
 
 constexpr uint64_t kDeltaMinIds = 1ull << 16;
 
+// processes of this job on this node (torchrun / SLURM-style launchers set it)
+uint64_t local_gpu_processes() {
+    const char* e = std::getenv("LOCAL_WORLD_SIZE");
+    const long v = e ? std::atol(e) : 1;
+    return v > 1 ? uint64_t(v) : 1;
+}
+
 }  // namespace
 
 void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
@@ -764,10 +771,11 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
         try {
             Lane lane(f, dev, b, minima != nullptr, score);
             lane.set_timed(false);
-            // one lane: the host cores are free to encode. Several lanes would
-            // share them, and N PCIe links reading 4 B per id beat one host
-            // encoding at 8 B of DRAM traffic per id.
-            lane.set_delta16(devs.size() == 1);
+            // one GPU feeding from this host: its cores are free to encode.
+            // With several (lanes here, or ranks of one job on this node,
+            // LOCAL_WORLD_SIZE) they share the host's DRAM, and N links reading
+            // 4 B per id beat encodes costing 8 B of DRAM traffic per id.
+            lane.set_delta16(devs.size() == 1 && local_gpu_processes() == 1);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
                 if (codes) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);
