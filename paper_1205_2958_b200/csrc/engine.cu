@@ -461,6 +461,12 @@ bool delta16_pays(const KernelFamily& kf) {
 
 constexpr uint64_t kDeltaMinIds = 1ull << 16;
 
+uint64_t chunk_idx_cap() {
+    const char* e = std::getenv("BBMH_CHUNK_IDS");  // developer knob (A/B timing)
+    const uint64_t v = e && *e ? std::strtoull(e, nullptr, 10) : 0;
+    return v >= (1u << 16) ? v : kChunkIdxCap;
+}
+
 // processes of this job on this node (torchrun / SLURM-style launchers set it)
 uint64_t local_gpu_processes() {
     const char* e = std::getenv("LOCAL_WORLD_SIZE");
@@ -752,7 +758,7 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     // slots' streams overlap one chunk's copy with another's kernel.
     const uint64_t total_ids = row_ptr[n] - row_ptr[0];
     const uint64_t idx_cap =
-        std::min<uint64_t>(kChunkIdxCap, std::max<uint64_t>(kMinSplitIds, total_ids / 4));
+        std::min<uint64_t>(chunk_idx_cap(), std::max<uint64_t>(kMinSplitIds, total_ids / 4));
     std::vector<uint64_t> bounds{0};
     for (uint64_t r = 0; r < n;) {
         uint64_t e = r + 1;
