@@ -98,10 +98,10 @@ bool encode_delta16(const uint64_t* row_ptr, uint64_t n, uint64_t base, const ui
                     uint16_t* deltas, uint32_t* exc_ptr, uint32_t* exc, uint64_t exc_cap,
                     uint64_t& nexc) {
     const uint64_t nidx = row_ptr[n] - base;
-    // tasks of >= 256 Ki ids, 4 per pool thread (taken dynamically: a thread
-    // the driver or the DMA interrupts holds nobody up), split at row
+    // tasks of >= 64 Ki ids, up to 4 per pool thread (taken dynamically: a
+    // thread the driver or the DMA interrupts holds nobody up), split at row
     // boundaries by id count
-    const unsigned T = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(4 * host_threads(), nidx >> 18)));
+    const unsigned T = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(4 * host_threads(), nidx >> 16)));
     std::vector<uint64_t> r0(T + 1);
     for (unsigned w = 0; w <= T; ++w) {
         const uint64_t target = base + nidx * w / T;

@@ -108,7 +108,7 @@ def test_delta_transfer_auto_on_webspam_shape(bb):
     """Default mode: 2U at k = 500 on webspam-shaped rows takes the 2-byte
     transfer (one decode launch per chunk) and agrees with the 4-byte one."""
     rng = np.random.default_rng(41)
-    rp, idx = random_csr(rng, 2000, 1 << 24, 3000, 4400)
+    rp, idx = random_csr(rng, 4000, 1 << 24, 3000, 4400)  # 4 chunks of ~3.7 Mi ids
     f = bb.Family(1, 1 << 24, 500, 42)
     os.environ.pop("BBMH_DELTA_H2D", None)
     l0 = bb.kernel_launches()
