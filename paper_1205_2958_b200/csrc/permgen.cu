@@ -4,14 +4,18 @@
 // per table j, tab[t] = t, then for t = D-1 .. 1 swap tab[t] with
 // tab[SplitMix64(keyed_u64(seed, 1, j, 0)).next_below(t + 1)] (prng.hpp:42-61).
 // Each shuffle is sequential; on the host it is bound by cache misses into a
-// 64 MB table (~0.4 s per table, 19 s for k = 500 on 16 cores). Here one
-// thread runs one table's shuffle, in windows of W swaps: the W draws are
-// computed and all 2W table entries loaded at once (W loads in flight per
-// thread instead of one), then the swaps are applied in order in registers,
-// forwarding values written earlier in the window, and stored. The result is
-// the same permutation, swap for swap. A draw that would take the rejection
-// branch of next_below (probability < 2^-32 per draw) marks its table, which
-// is then rebuilt on the host.
+// 64 MB table (~0.4 s per table, 19 s for k = 500 on 16 cores).
+//
+// Here one warp runs one table's shuffle, 32 swaps per step. SplitMix64's
+// i-th draw is mix64(seed + (i+1)·φ), so the 32 lanes draw their swaps'
+// partners at once. Swap i touches positions t0-i and r_i. When no r_i falls
+// inside the step's own positions [t0-31, t0] and no two r_i are equal, the
+// 32 swaps touch 64 distinct entries and commute: every lane loads its two
+// entries, then stores them exchanged. Otherwise (about 800 of the 524 K steps
+// of a 2^24 table, nearly all near its end) lane 0 applies the step's swaps in
+// order. The result is the same permutation, swap for swap. A draw that would
+// take the rejection branch of next_below (probability < 2^-32 per draw)
+// marks its table, which is then rebuilt on the host.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -42,65 +46,64 @@ __global__ void perm_init_kernel(uint32_t* __restrict__ perm, uint64_t dim, uint
         perm[i] = uint32_t(i % dim);
 }
 
-template <int W>
-__global__ void __launch_bounds__(32) perm_shuffle_kernel(uint32_t* __restrict__ perm, uint64_t dim,
-                                                         uint32_t k, const uint64_t* __restrict__ seeds,
-                                                         uint32_t* __restrict__ host_redo) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= k) return;
+__global__ void __launch_bounds__(128) perm_shuffle_warp_kernel(uint32_t* __restrict__ perm, uint64_t dim,
+                                                                uint32_t k, const uint64_t* __restrict__ seeds,
+                                                                uint32_t* __restrict__ host_redo) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (j >= k) return;  // whole warps
     uint32_t* tab = perm + size_t(j) * dim;
-    uint64_t state = seeds[j];
+    const uint64_t seed = seeds[j];
+    uint64_t drawn = 0;  // draws used by earlier steps
     for (uint64_t t0 = dim - 1; t0 > 0;) {
-        const int w = t0 < uint64_t(W) ? int(t0) : W;
-        uint32_t r[W], A[W], B[W];
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (i < w) {
-                const uint64_t bound = t0 - i + 1;
-                state += kPhi;
-                const uint64_t v = dmix64(state);
-                if ((bound & (bound - 1)) == 0) {
-                    r[i] = uint32_t(v & (bound - 1));
-                } else {
-                    // next_below's rejection: v >= UINT64_MAX - UINT64_MAX % bound,
-                    // only possible in the top `bound` values of the range
-                    if ((v >> 32) == 0xffffffffull && v >= ~0ull - (~0ull % bound)) {
-                        host_redo[j] = 1;
-                        return;
-                    }
-                    r[i] = uint32_t(v % bound);
+        const uint32_t w = t0 < 32 ? uint32_t(t0) : 32u;  // swaps t = t0, t0-1, ..., t0-w+1
+        const bool act = lane < w;
+        const uint64_t t = t0 - lane;
+        uint64_t r = 0;
+        bool rejected = false;
+        if (act) {
+            const uint64_t bound = t + 1;
+            const uint64_t v = dmix64(seed + (drawn + lane + 1) * kPhi);
+            if ((bound & (bound - 1)) == 0) {
+                r = v & (bound - 1);
+            } else {
+                // next_below's rejection: v >= UINT64_MAX - UINT64_MAX % bound,
+                // only possible in the top `bound` values of the range
+                rejected = (v >> 32) == 0xffffffffull && v >= ~0ull - (~0ull % bound);
+                r = v % bound;
+            }
+        }
+        if (__any_sync(0xffffffffu, rejected)) {
+            if (lane == 0) host_redo[j] = 1;
+            return;
+        }
+        const bool in_step = act && r + w > t0;  // r in [t0-w+1, t0]
+        const unsigned same = __match_any_sync(0xffffffffu, act ? r : ~0ull - lane);
+        const bool dup = act && __popc(same) > 1;
+        if (!__any_sync(0xffffffffu, in_step || dup)) {
+            uint32_t a = 0, b = 0;
+            if (act) {
+                a = tab[t];
+                b = tab[r];
+            }
+            if (act) {
+                tab[t] = b;
+                tab[r] = a;
+            }
+        } else {
+            for (uint32_t i = 0; i < w; ++i) {
+                const uint64_t ri = __shfl_sync(0xffffffffu, r, int(i));
+                if (lane == 0) {
+                    const uint64_t ti = t0 - i;
+                    const uint32_t x = tab[ti];
+                    tab[ti] = tab[ri];
+                    tab[ri] = x;
                 }
             }
         }
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (i < w) {
-                A[i] = tab[t0 - i];
-                B[i] = tab[r[i]];
-            }
-        }
-        // the window's swaps in order; lp/lv log the writes (later entries win)
-        uint32_t lp[2 * W], lv[2 * W];
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            if (i < w) {
-                const uint32_t t = uint32_t(t0 - i);
-                uint32_t vt = A[i], vr = B[i];
-#pragma unroll
-                for (int q = 0; q < 2 * i; ++q) {
-                    vt = lp[q] == t ? lv[q] : vt;
-                    vr = lp[q] == r[i] ? lv[q] : vr;
-                }
-                lp[2 * i] = t;
-                lv[2 * i] = vr;
-                lp[2 * i + 1] = r[i];
-                lv[2 * i + 1] = vt;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 2 * W; ++q)
-            if (q < 2 * w) tab[lp[q]] = lv[q];
-        t0 -= uint64_t(w);
+        __syncwarp();  // this step's stores before the next step's loads, across lanes
+        drawn += w;
+        t0 -= w;
     }
 }
 
@@ -146,7 +149,7 @@ bool build_perm_tables_gpu(Family& f) {
     cudaMemcpy(d_seeds, seeds.data(), k * 8, cudaMemcpyHostToDevice);
     cudaMemset(d_redo, 0, k * 4);
     perm_init_kernel<<<2048, 256>>>(d_perm, dim, dim * k);
-    perm_shuffle_kernel<16><<<unsigned((k + 31) / 32), 32>>>(d_perm, dim, uint32_t(k), d_seeds, d_redo);
+    perm_shuffle_warp_kernel<<<unsigned((k + 3) / 4), 128>>>(d_perm, dim, uint32_t(k), d_seeds, d_redo);
     count_launches(2);
     std::vector<uint32_t> redo(k, 0);
     if (cudaDeviceSynchronize() != cudaSuccess ||

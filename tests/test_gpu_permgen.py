@@ -35,3 +35,19 @@ def test_gpu_built_tables_match_reference(bb, port, dim, k):
         os.environ.pop("BBMH_GPU_PERMGEN")
     port.destroy(h)
     f.close()
+
+
+@pytest.mark.parametrize("dim,k", [(1 << 22, 16), (5_000_011, 4)])
+def test_gpu_built_tables_match_reference_on_whole_slices(bb, port, dim, k):
+    """Every entry of the tables' first and last 2^16 positions (where the
+    warp shuffle's serial steps and its parallel steps meet), read through
+    single-id documents: minima[t][j] = table_j[t]."""
+    f = bb.Family(0, dim, k, 7, 0, 1 << 34)
+    st, h = port.family(0, dim, k, 7, 0, 1 << 34)
+    ts = np.concatenate([np.arange(1 << 16), np.arange(dim - (1 << 16), dim)]).astype(np.uint32)
+    rp = np.arange(ts.size + 1, dtype=np.uint64)
+    _, minima, _ = f.sketch_csr(rp, ts, 8, want_minima=True)
+    s, _, m2, _ = port.sketch_csr(h, k, rp, ts, 8)
+    assert s == 0 and np.array_equal(minima, m2)
+    port.destroy(h)
+    f.close()
