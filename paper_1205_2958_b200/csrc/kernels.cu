@@ -28,6 +28,7 @@
 #include <mutex>
 #include <tuple>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -557,6 +558,12 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
         sms = it->second.first;
         occ = it->second.second;
     }
+    // One-warp CTAs of the wide-J 2U shapes (k = 200: J = 7; k = 256: J = 8)
+    // run 8% faster at 20 CTAs per SM than at the 24 shared memory allows;
+    // the thin-J ones (k <= 128) run 8% slower with that cap
+    // (tools/grid_2u_cap.json, profiles/r11/ksweep_cap.txt).
+    if (SCHEME == S_2U && J >= 7 && sh.tpb == 32 && env_int("BBMH_TUNE_SMEM_CAP", 1))
+        occ = std::min(occ, 20);
     const int ctas_env = env_int("BBMH_TUNE_CTAS_PER_SM", 0);
     if (ctas_env > 0 && ctas_env < occ) occ = ctas_env;
     // persistent: one wave of CTAs per j-tile, each looping over documents
@@ -669,7 +676,8 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     }
     // developer tuning knobs (not part of the ABI)
     const int J = env_int("BBMH_TUNE_J", 0), tpb = env_int("BBMH_TUNE_TPB", 0);
-    if ((J == 1 || J == 2 || J == 4 || J == 8) && tpb >= 32 && tpb <= 256 && tpb % 32 == 0) {
+    if ((J == 1 || J == 2 || J == 4 || J == 8 || (J == 7 && scheme == S_2U)) && tpb >= 32 &&
+        tpb <= 256 && tpb % 32 == 0) {
         best.J = J;
         best.tpb = tpb;
         best.jtile = (uint32_t)(J * tpb);

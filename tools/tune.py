@@ -16,10 +16,11 @@ from paper_1205_2958_b200 import bbmh  # noqa: E402
 
 def main():
     n = int(os.environ.get("TUNE_DOCS", "200000"))
+    K = int(os.environ.get("TUNE_K", bench.K))
     schemes = os.environ.get("TUNE_SCHEMES", "2u").split(",")
     dev = torch.device("cuda", 0)
     d_rp, d_idx = bench.make_corpus_device(torch, n, bench.NNZ, bench.D_WEBSPAM, 1, dev)
-    cb = (bench.K * bench.B + 7) // 8
+    cb = (K * bench.B + 7) // 8
     d_codes = torch.empty(n * cb, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
     grid = json.loads(os.environ.get("TUNE_GRID", "[]")) or [
@@ -28,7 +29,7 @@ def main():
             [(4, 128), (8, 64), (2, 256), (1, 512 // 2)], [1024, 2048, 4096], [0])]
     for scheme in schemes:
         sid, dim = bench.SCHEMES[scheme]
-        fam = bbmh.Family(sid, dim, bench.K, bench.SEED)
+        fam = bbmh.Family(sid, dim, K, bench.SEED)
         for k_ in ("J", "TPB", "TILE", "CTAS_PER_SM", "G"):
             os.environ.pop("BBMH_TUNE_" + k_, None)
         fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, bench.B,
@@ -36,10 +37,15 @@ def main():
         torch.cuda.synchronize()
         ref_codes = d_codes.clone()
         for g in grid:
-            os.environ["BBMH_TUNE_J"] = str(g["J"])
-            os.environ["BBMH_TUNE_TPB"] = str(g["TPB"])
+            if g.get("J", 0):
+                os.environ["BBMH_TUNE_J"] = str(g["J"])
+                os.environ["BBMH_TUNE_TPB"] = str(g["TPB"])
+            else:  # the library's own shape for this k
+                os.environ.pop("BBMH_TUNE_J", None)
+                os.environ.pop("BBMH_TUNE_TPB", None)
             os.environ["BBMH_TUNE_TILE"] = str(g["TILE"])
             os.environ["BBMH_TUNE_CTAS_PER_SM"] = str(g.get("CTAS", 0))
+            os.environ["BBMH_TUNE_SMEM_CAP"] = str(g.get("SMEM_CAP", 1))
             os.environ["BBMH_TUNE_G"] = str(g.get("G", 4))
 
             def step():
@@ -58,8 +64,8 @@ def main():
             ms = e0.elapsed_time(e1) / reps
             same = bool(torch.equal(d_codes, ref_codes))
             d_codes.zero_()
-            evals = n * bench.NNZ * bench.K
-            print(json.dumps({"scheme": scheme, **g, "ms": round(ms, 3),
+            evals = n * bench.NNZ * K
+            print(json.dumps({"scheme": scheme, "k": K, **g, "ms": round(ms, 3),
                               "tevals": round(evals / ms / 1e9, 3), "codes_match_default": same}), flush=True)
 
 
