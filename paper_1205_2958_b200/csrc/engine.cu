@@ -565,9 +565,15 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
         BBMH_CUDA(cudaGetLastError());
     }
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev1, s.st));
-    d2h(h + s.off_err, d + s.off_err, s.blk_end - s.off_err, s.st);
+    if (job.codes_out) {  // codes straight into the caller's page-locked buffer
+        d2h(h + s.off_err, d + s.off_err, s.off_codes - s.off_err, s.st);
+        if (n && cb_) d2h(job.codes_out, d + s.off_codes, n * cb_, s.st);
+    } else {
+        d2h(h + s.off_err, d + s.off_err, s.blk_end - s.off_err, s.st);
+    }
     BBMH_CUDA(cudaEventRecord(s.done, s.st));
     s.busy = true;
+    trace("lane: enqueued");
 }
 
 void Lane::enqueue(Slot& s, const ChunkJob& job) {
@@ -628,7 +634,7 @@ ChunkResult Lane::finish(Slot& s) {
     if (s.packed) {
         std::memcpy(&herr, s.h_blk + s.off_err, sizeof(int));
         std::memcpy(&hbad, s.h_blk + s.off_err + 8, sizeof(hbad));
-        r.codes = s.h_blk + s.off_codes;
+        r.codes = s.job.codes_out ? s.job.codes_out : s.h_blk + s.off_codes;
         r.minima = nullptr;
         r.flags = s.h_blk + s.off_flags;
         r.scores = d_w_ ? reinterpret_cast<const double*>(s.h_blk + s.off_scores) : nullptr;
@@ -753,6 +759,8 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
             return;
     }
 
+    // a page-locked output buffer takes the codes' D2H directly
+    const bool codes_pinned = codes && !minima && is_pinned(codes) && is_pinned(codes + n * cb - 1);
     // chunk boundaries: <= chunk_docs rows, <= kChunkIdxCap ids (unless one row is larger)
     uint64_t cap_docs = chunk_docs_setting();
     if (minima) cap_docs = std::max<uint64_t>(1, std::min<uint64_t>(cap_docs, kChunkMinimaBytes / (8ull * f.k)));
@@ -787,10 +795,11 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
             lane.set_delta16(devs.size() == 1 && local_gpu_processes() == 1);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
-                if (codes) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);
+                if (codes && res.codes != codes + r0 * cb) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);
                 if (scores) std::memcpy(scores + r0, res.scores, res.n * sizeof(double));
                 if (minima) host_memcpy(minima + r0 * f.k, res.minima, res.n * f.k * 8);
                 if (flags) std::memcpy(flags + r0, res.flags, res.n);
+                trace("host: chunk copied out");
             };
             for (uint64_t c; !abort.load() && (c = next.fetch_add(1)) < nchunks;) {
                 ChunkJob job;
@@ -800,6 +809,7 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
                 job.indices = indices + row_ptr[bounds[c]];
                 job.n = bounds[c + 1] - bounds[c];
                 job.pinned_input = pinned;
+                if (codes_pinned) job.codes_out = codes + bounds[c] * cb;
                 lane.submit(job, done);
             }
             lane.drain(done);

@@ -62,6 +62,8 @@ struct ChunkJob {
     const uint32_t* indices = nullptr;  // host, starting at index_base
     uint64_t n = 0;
     bool pinned_input = false;        // row_ptr/indices already page-locked
+    uint8_t* codes_out = nullptr;     // page-locked host destination of the chunk's codes:
+                                      // the D2H lands there (no minima chunks)
 };
 
 struct ChunkResult {

@@ -136,7 +136,7 @@ unsigned host_threads() { return pool().size(); }
 void host_parallel(unsigned tasks, const std::function<void(unsigned)>& fn) { pool().run(tasks, fn); }
 
 void host_memcpy(void* dst, const void* src, size_t n) {
-    const size_t T = std::min<size_t>(host_threads(), n >> 20);
+    const size_t T = std::min<size_t>(host_threads(), n >> 18);
     if (T <= 1) {
         std::memcpy(dst, src, n);
         return;

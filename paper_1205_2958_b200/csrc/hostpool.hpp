@@ -17,7 +17,7 @@ unsigned host_threads();
 // first exception thrown by a task is rethrown here.
 void host_parallel(unsigned tasks, const std::function<void(unsigned)>& fn);
 
-// memcpy split over the pool in pieces of >= 1 MiB (one thread copies ~10 GB/s).
+// memcpy split over the pool in pieces of >= 256 KiB (one thread copies ~10 GB/s).
 void host_memcpy(void* dst, const void* src, size_t n);
 
 }  // namespace bbmh
