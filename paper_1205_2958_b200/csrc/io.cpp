@@ -693,11 +693,16 @@ private:
 
     void compact_if_needed() {}
 
-    // pread of [file_off_, file_off_ + n) into p, split over up to 8 threads
+    // pread of [file_off_, file_off_ + n) into p, split over up to 16 threads
     // (one thread copies ~10 GB/s out of the page cache); returns bytes read.
     size_t read_at(char* p, size_t n) {
         const int fd = fileno(f_);
-        const unsigned T = n >= (size_t(16) << 20) ? std::min(8u, threads_) : 1u;
+        static const unsigned kReadThreads = [] {
+            const char* e = std::getenv("BBMH_READ_THREADS");  // developer knob (A/B timing)
+            const int v = e && *e ? std::atoi(e) : 0;
+            return v > 0 ? unsigned(v) : 16u;  // 8 -> 16 threads: 15.7 -> 17.5 GB/s of text
+        }();
+        const unsigned T = n >= (size_t(16) << 20) ? std::min(kReadThreads, threads_) : 1u;
         std::vector<size_t> got(T, 0);
         std::vector<int> err(T, 0);
         auto work = [&](unsigned w) {
