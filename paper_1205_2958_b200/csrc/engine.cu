@@ -483,7 +483,7 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     const uint64_t n = job.n;
     const int dmode = delta16_mode();
     bool delta = dmode != 0 && nidx > 0 &&
-                 (dmode == 1 || (delta16_ && nidx >= kDeltaMinIds && delta16_pays(df_->kf) &&
+                 (dmode == 1 || (delta16_ && !job.ids_as_is && nidx >= kDeltaMinIds && delta16_pays(df_->kf) &&
                                  delta16_worthwhile(job.row_ptr, n, job.index_base, job.indices)));
     const bool inline_ids = !job.pinned_input;
     const size_t raw_err = align16(align16((n + 1) * sizeof(uint64_t)) + (inline_ids ? nidx * sizeof(uint32_t) : 0));
@@ -759,6 +759,14 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
             return;
     }
 
+    // Mixing transfers: encoded chunks cost 8 B of host DRAM traffic per id
+    // and 2 B of PCIe, raw ones 4 B of each. With the encode bound by host
+    // DRAM and the link idle half the time, sending some chunks raw moves
+    // more ids per second than either alone.
+    const uint64_t raw_every = [] {
+        const char* e = std::getenv("BBMH_DELTA_RAW_EVERY");  // developer knob (A/B timing)
+        return e && *e ? std::strtoull(e, nullptr, 10) : uint64_t(0);
+    }();
     // a page-locked output buffer takes the codes' D2H directly
     const bool codes_pinned = codes && !minima && is_pinned(codes) && is_pinned(codes + n * cb - 1);
     // chunk boundaries: <= chunk_docs rows, <= kChunkIdxCap ids (unless one row is larger)
@@ -810,6 +818,9 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
                 job.n = bounds[c + 1] - bounds[c];
                 job.pinned_input = pinned;
                 if (codes_pinned) job.codes_out = codes + bounds[c] * cb;
+                // every raw_every-th chunk crosses as 4-byte ids: its DMA needs
+                // no host cores and runs while the others are encoded
+                job.ids_as_is = raw_every && c % raw_every == raw_every - 1;
                 lane.submit(job, done);
             }
             lane.drain(done);

@@ -64,6 +64,7 @@ struct ChunkJob {
     bool pinned_input = false;        // row_ptr/indices already page-locked
     uint8_t* codes_out = nullptr;     // page-locked host destination of the chunk's codes:
                                       // the D2H lands there (no minima chunks)
+    bool ids_as_is = false;           // send this chunk's ids as they are (see delta.hpp)
 };
 
 struct ChunkResult {
