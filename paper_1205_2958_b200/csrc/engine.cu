@@ -482,10 +482,10 @@ uint64_t local_gpu_processes() {
 void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     const uint64_t n = job.n;
     const int dmode = delta16_mode();
-    bool delta = dmode != 0 && nidx > 0 &&
+    bool delta = dmode != 0 && nidx > 0 && !job.d_indices &&
                  (dmode == 1 || (delta16_ && !job.ids_as_is && nidx >= kDeltaMinIds && delta16_pays(df_->kf) &&
                                  delta16_worthwhile(job.row_ptr, n, job.index_base, job.indices)));
-    const bool inline_ids = !job.pinned_input;
+    const bool inline_ids = !job.pinned_input && !job.d_indices;
     const size_t raw_err = align16(align16((n + 1) * sizeof(uint64_t)) + (inline_ids ? nidx * sizeof(uint32_t) : 0));
     const size_t d_exc_ptr = align16((n + 1) * sizeof(uint64_t));
     const size_t d_deltas = align16(d_exc_ptr + (n + 1) * sizeof(uint32_t));
@@ -538,11 +538,13 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     std::memset(h + s.off_err, 0, 8);
     std::memset(h + s.off_err + 8, 0xff, 8);
     const uint32_t* d_ids = reinterpret_cast<const uint32_t*>(d + s.off_ids);
-    if (delta || (!inline_ids && nidx)) {
+    if (job.d_indices) {
+        d_ids = job.d_indices;
+    } else if (delta || (!inline_ids && nidx)) {
         grow_device(s.d_idx, s.cap_idx, nidx + kIdsSlack);
         d_ids = s.d_idx;
     }
-    if (!delta && !inline_ids && nidx)
+    if (!job.d_indices && !delta && !inline_ids && nidx)
         h2d(s.d_idx, job.indices, nidx * sizeof(uint32_t), s.st);
     h2d(s.d_blk, h, s.off_err + 16, s.st);
     if (delta) {
@@ -588,20 +590,20 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
         return;
     }
     s.packed = false;
-    reserve(s, n, nidx, stage);
+    reserve(s, n, job.d_indices ? 0 : nidx, stage && !job.d_indices);
     // row_ptr always goes through the slot's pinned mirror (small)
     std::memcpy(s.h_rp, job.row_ptr, (n + 1) * sizeof(uint64_t));
     h2d(s.d_rp, s.h_rp, (n + 1) * sizeof(uint64_t), s.st);
     const uint32_t* src = job.indices;
-    if (stage && nidx) {
+    if (stage && nidx && !job.d_indices) {
         host_memcpy(s.h_idx, job.indices, nidx * sizeof(uint32_t));
         src = s.h_idx;
     }
-    if (nidx)
+    if (nidx && !job.d_indices)
         h2d(s.d_idx, src, nidx * sizeof(uint32_t), s.st);
     BBMH_CUDA(cudaMemsetAsync(s.d_err, 0, sizeof(int), s.st));
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
-    launch_sketch(df_->kf, s.d_rp, job.index_base, s.d_idx, n, b_, s.d_codes,
+    launch_sketch(df_->kf, s.d_rp, job.index_base, job.d_indices ? job.d_indices : s.d_idx, n, b_, s.d_codes,
                   want_minima_ ? s.d_min : nullptr, s.d_flags, s.d_err, s.st);
     BBMH_CUDA(cudaGetLastError());
     if (d_w_) {  // fused scoring on the device-resident codes (score.cu)

@@ -65,6 +65,8 @@ struct ChunkJob {
     uint8_t* codes_out = nullptr;     // page-locked host destination of the chunk's codes:
                                       // the D2H lands there (no minima chunks)
     bool ids_as_is = false;           // send this chunk's ids as they are (see delta.hpp)
+    const uint32_t* d_indices = nullptr;  // the ids already on the lane's device (then
+                                          // `indices` is not read); granule slack required
 };
 
 struct ChunkResult {

@@ -43,6 +43,13 @@ void write_all(FILE* f, const void* data, size_t n) {
 
 Batch::~Batch() {
     if (ids) cudaFreeHost(ids);
+    if (d_ids) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(d_dev);
+        cudaFree(d_ids);
+        cudaSetDevice(cur);
+    }
 }
 
 void Batch::reserve_ids(uint64_t cap) {
@@ -52,11 +59,39 @@ void Batch::reserve_ids(uint64_t cap) {
     if (cudaMallocHost(&p, std::max<uint64_t>(cap, 1) * sizeof(uint32_t)) != cudaSuccess)
         fail(Errc::Cuda, "cudaMallocHost failed for a loader batch");
     if (ids) {
-        std::memcpy(p, ids, nids() * sizeof(uint32_t));
+        // (with device-resident ids the host array may be shorter than nids())
+        std::memcpy(p, ids, std::min(nids(), cap_ids) * sizeof(uint32_t));
         cudaFreeHost(ids);
     }
     ids = p;
     cap_ids = cap;
+}
+
+uint32_t* Batch::reserve_device_ids(int dev, uint64_t cap) {
+    constexpr uint64_t kSlack = 16;  // the sketch kernel's bulk copies read whole 16-byte granules
+    if (d_ids && d_dev == dev && cap + kSlack <= d_cap) return d_ids;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    const uint64_t ncap = std::max<uint64_t>(cap + kSlack, d_dev == dev ? d_cap + d_cap / 2 : 0);
+    uint32_t* p = nullptr;
+    if (cudaMalloc(&p, ncap * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaSetDevice(cur);
+        fail(Errc::Cuda, "cudaMalloc failed for a loader batch");
+    }
+    if (d_ids && d_dev == dev && d_valid) cudaMemcpy(p, d_ids, d_valid * sizeof(uint32_t), cudaMemcpyDeviceToDevice);
+    if (d_ids) {
+        cudaSetDevice(d_dev);
+        cudaFree(d_ids);
+        cudaSetDevice(dev);
+    }
+    if (d_dev != dev) d_valid = 0;
+    d_ids = p;
+    d_cap = ncap;
+    d_dev = dev;
+    cudaSetDevice(cur);
+    return d_ids;
 }
 
 namespace {
@@ -400,7 +435,35 @@ public:
         return_text_res(std::move(res_));
     }
 
+    int parser_device() const override { return gpu_ ? gpu_->device() : -1; }
+
     bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) override {
+        if (!gpu_) b.want_device_ids = false;
+        const bool any = fill_rows(b, max_docs, max_ids);
+        if (b.want_device_ids) upload_host_ids(b);  // every id on the device
+        return any;
+    }
+
+private:
+    // The CPU parser's rows [d_valid, nids()) of a device-resident batch, up.
+    void upload_host_ids(Batch& b) {
+        if (b.d_valid >= b.nids()) return;
+        const int dev = gpu_->device();
+        b.reserve_device_ids(dev, b.nids());
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        const cudaError_t e = cudaMemcpy(b.d_ids + b.d_valid, b.ids + b.d_valid,
+                                         (b.nids() - b.d_valid) * sizeof(uint32_t), cudaMemcpyHostToDevice);
+        cudaSetDevice(cur);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            fail(Errc::Cuda, std::string("upload of a loader batch failed: ") + cudaGetErrorString(e));
+        }
+        b.d_valid = b.nids();
+    }
+
+    bool fill_rows(Batch& b, uint64_t max_docs, uint64_t max_ids) {
         bool any = false;
         while (b.n < max_docs && (b.nids() < max_ids || b.n == 0)) {
             if (gpu_ && pos_ >= cpu_until_) {
@@ -428,7 +491,6 @@ public:
         return any;
     }
 
-private:
     static constexpr size_t kBlock = size_t(64) << 20;
     static constexpr size_t kGpuBlock = size_t(32) << 20;
 
@@ -566,11 +628,21 @@ private:
             if (need > b.cap_ids) b.reserve_ids(need + (1u << 20));
             return b.ids;
         };
+        // device-resident ids: the rows the CPU parser took go up first, so
+        // the device holds a prefix [0, d_valid) and this block extends it
+        const bool dev = b.want_device_ids;
+        DeviceIdsOut dout;
+        if (dev) {
+            upload_host_ids(b);
+            dout.reserve = [&](uint64_t need) { return b.reserve_device_ids(gpu_->device(), need); };
+            dout.base = b.nids();
+        }
         GpuParseResult r;
         try {
             r = gpu_->parse(buf_->data() + pos_, cut - pos_, at_eof, b.nids(), rows_left,
                             empty ? UINT64_MAX : ids_left, reserve, b.row_ptr, b.labels, key,
-                            next ? buf_->data() + cut : nullptr, next ? ncut - cut : 0, nkey);
+                            next ? buf_->data() + cut : nullptr, next ? ncut - cut : 0, nkey,
+                            dev ? &dout : nullptr);
         } catch (...) {
             if (ahead.joinable()) ahead.join();
             throw;
@@ -607,6 +679,7 @@ private:
             trace(msg);
         }
         b.n += r.rows;
+        if (dev) b.d_valid = b.nids();
         line_no_ += r.lines;
         lines_seen_ += r.lines;
         bytes_seen_ += r.bytes;

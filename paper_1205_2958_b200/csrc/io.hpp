@@ -28,13 +28,28 @@ struct Batch {
     uint32_t* ids = nullptr;  // pinned
     uint64_t cap_ids = 0;
     std::vector<float> vals;  // per-id values (LibSVM value mode only)
+
+    // Device-resident ids. A consumer on the GPU that parses LibSVM text sets
+    // want_device_ids: the parser then writes the ids straight into d_ids on
+    // d_dev (no D2H, and no H2D by the lane later), and when fill() returns
+    // ids [0, nids()) are all valid there; `ids` on the host then holds only
+    // the rows the CPU parser took (blocks outside the device grammar).
+    bool want_device_ids = false;
+    int d_dev = -1;
+    uint32_t* d_ids = nullptr;
+    uint64_t d_cap = 0;
+    uint64_t d_valid = 0;  // ids [0, d_valid) are on the device
+
     ~Batch();
     void reserve_ids(uint64_t cap);  // keeps contents
+    // device buffer of >= cap ids (+ the kernels' granule slack) on `dev`; keeps [0, d_valid)
+    uint32_t* reserve_device_ids(int dev, uint64_t cap);
     void clear() {
         n = 0;
         row_ptr.assign(1, 0);
         labels.clear();
         vals.clear();
+        d_valid = 0;
     }
     uint64_t nids() const { return row_ptr.back(); }
 };
@@ -46,6 +61,9 @@ public:
     // (a single row may exceed max_ids). Returns false at end of input with
     // no record appended. Throws bbmh::Error with the reference's messages.
     virtual bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) = 0;
+    // The GPU that parses this corpus (-1: none): batches filled with
+    // want_device_ids get their ids there.
+    virtual int parser_device() const { return -1; }
 };
 
 // open_corpus: sniff the "BBCV" magic, else LibSVM text (dataio.cpp:257-264).

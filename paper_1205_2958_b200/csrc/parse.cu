@@ -289,7 +289,8 @@ GpuLibsvmParser::~GpuLibsvmParser() {
 
 GpuParseResult GpuLibsvmParser::run(const char* text, uint64_t len, bool at_eof, uint64_t max_rows,
                                     uint64_t max_ids, uint64_t key, const char* next_text,
-                                    uint64_t next_len, uint64_t next_key) {
+                                    uint64_t next_len, uint64_t next_key,
+                                    const DeviceIdsOut* dev_out) {
     GpuParseResult r;
     if (len == 0 || len >= (1ull << 32)) return r;
     BBMH_CUDA(cudaSetDevice(device_));
@@ -352,17 +353,23 @@ GpuParseResult GpuLibsvmParser::run(const char* text, uint64_t len, bool at_eof,
     uint64_t cl7 = cap_lines_;
     grow_dev(d_labels_, cl7, nlines + 1);
     cap_lines_ = std::min<uint64_t>({cl, cl2, cl3, cl4, cl5, cl6, cl7});
-    uint64_t ci = cap_ids_;
-    grow_dev(d_ids_, ci, ncol + 1);
-    cap_ids_ = ci;
+    if (dev_out) {  // straight into the caller's device buffer
+        ids_dst_ = dev_out->reserve(dev_out->base + ncol + 1) + dev_out->base;
+        BBMH_CUDA(cudaSetDevice(device_));
+    } else {
+        uint64_t ci = cap_ids_;
+        grow_dev(d_ids_, ci, ncol + 1);
+        cap_ids_ = ci;
+        ids_dst_ = d_ids_;
+    }
     BBMH_CUDA(cudaMemsetAsync(d_line_tok_, 0, nlines * sizeof(uint32_t), st_));
     seg_emit<<<unsigned(nseg), kTpb, 0, st_>>>(d_text_, len, nchunk, at_eof ? 1 : 0, d_seg_,
-                                               d_line_end_, d_colons_before_, d_line_tok_, d_ids_,
+                                               d_line_end_, d_colons_before_, d_line_tok_, ids_dst_,
                                                d_flags_);
     BBMH_CUDA(cudaGetLastError());
     const uint64_t warps_tpb = 256;
     line_check<<<unsigned((nlines * 32 + warps_tpb - 1) / warps_tpb), unsigned(warps_tpb), 0, st_>>>(
-        d_text_, uint32_t(nlines), d_line_end_, d_colons_before_, d_line_tok_, d_ids_,
+        d_text_, uint32_t(nlines), d_line_end_, d_colons_before_, d_line_tok_, ids_dst_,
         d_row_of_line_, d_line_label_, d_flags_);
     BBMH_CUDA(cudaGetLastError());
     tmp = 0;
@@ -444,8 +451,8 @@ void GpuLibsvmParser::cancel_prefetch() {
 void GpuLibsvmParser::fetch(uint32_t* ids_out, uint64_t id_base, std::vector<uint64_t>& row_ptr,
                             std::vector<int8_t>& labels, const GpuParseResult& r) {
     BBMH_CUDA(cudaSetDevice(device_));
-    if (r.ids)
-        BBMH_CUDA(cudaMemcpyAsync(ids_out, d_ids_, r.ids * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+    if (r.ids && ids_out)  // (null: the ids stay on the device)
+        BBMH_CUDA(cudaMemcpyAsync(ids_out, ids_dst_, r.ids * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                   st_));
     const size_t r0 = row_ptr.size(), l0 = labels.size();
     row_ptr.resize(r0 + r.rows);

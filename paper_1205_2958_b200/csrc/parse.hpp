@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 namespace bbmh {
@@ -26,6 +27,14 @@ struct GpuParseResult {
     uint64_t rows = 0;         // non-blank lines
     uint64_t ids = 0;          // ids written
     uint64_t bytes = 0;        // bytes consumed: the block, or the prefix that fit the budget
+};
+
+// Device-resident output of a block's ids: reserve(n) returns a device buffer
+// (on the parser's device) of at least n ids; entries from `base` on receive
+// the block's ids, which are then not copied to the host.
+struct DeviceIdsOut {
+    std::function<uint32_t*(uint64_t)> reserve;
+    uint64_t base = 0;
 };
 
 class GpuLibsvmParser {
@@ -50,13 +59,15 @@ public:
                          uint64_t max_rows, uint64_t max_ids, Reserve&& reserve,
                          std::vector<uint64_t>& row_ptr, std::vector<int8_t>& labels,
                          uint64_t key, const char* next_text = nullptr, uint64_t next_len = 0,
-                         uint64_t next_key = 0) {
-        GpuParseResult r = run(text, len, at_eof, max_rows, max_ids, key, next_text, next_len, next_key);
+                         uint64_t next_key = 0, const DeviceIdsOut* dev_out = nullptr) {
+        GpuParseResult r = run(text, len, at_eof, max_rows, max_ids, key, next_text, next_len,
+                               next_key, dev_out);
         if (!r.ok) return r;
-        uint32_t* ids_out = reserve(id_base + r.ids);
-        fetch(ids_out + id_base, id_base, row_ptr, labels, r);
+        uint32_t* ids_out = dev_out ? nullptr : reserve(id_base + r.ids) + id_base;
+        fetch(ids_out, id_base, row_ptr, labels, r);
         return r;
     }
+    int device() const { return device_; }
 
     // Starts the H2D copy of a block on a copy stream; parse() of the same
     // (key, len) then skips its own copy. The host bytes must stay untouched
@@ -69,7 +80,7 @@ public:
 private:
     GpuParseResult run(const char* text, uint64_t len, bool at_eof, uint64_t max_rows,
                        uint64_t max_ids, uint64_t key, const char* next_text, uint64_t next_len,
-                       uint64_t next_key);
+                       uint64_t next_key, const DeviceIdsOut* dev_out);
     void fetch(uint32_t* ids_out, uint64_t id_base, std::vector<uint64_t>& row_ptr,
                std::vector<int8_t>& labels, const GpuParseResult& r);
     void grow(uint64_t len);
@@ -90,7 +101,8 @@ private:
     uint32_t* d_line_tok_ = nullptr;        // tokens per line
     uint32_t* d_row_of_line_ = nullptr;     // 1 for non-blank lines, then scanned
     int8_t* d_line_label_ = nullptr;
-    uint32_t* d_ids_ = nullptr;
+    uint32_t* d_ids_ = nullptr;             // ids (host-bound blocks)
+    uint32_t* ids_dst_ = nullptr;           // where the current block's ids went
     uint64_t* d_row_end_ = nullptr;         // rows: end (exclusive) in ids
     int8_t* d_labels_ = nullptr;
     uint32_t* d_flags_ = nullptr;           // [0] bad, [1] rows, [2] lines, [3] ids, [4..8) prefix

@@ -10,6 +10,7 @@
 #include "pipeline.hpp"
 
 #include <chrono>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -201,6 +202,12 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
     const uint64_t max_docs = chunk_docs_setting();
     const bool b_ok = b >= 1 && b <= 32;
 
+    // One GPU that also parses the text: its batches keep their ids on the
+    // device (no D2H after parsing, no H2D before sketching).
+    const bool device_ids = devs.size() == 1 && reader.parser_device() == devs[0] && [] {
+        const char* e = std::getenv("BBMH_DEVICE_IDS");  // developer knob (A/B timing)
+        return !(e && *e == '0');
+    }();
     const size_t nbatches = 3 * devs.size() + 3;
     BatchLease storage(nbatches);  // pinned batches reused across calls
     trace("stream: batches leased");
@@ -228,6 +235,7 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
                 if (!free_q.pop(bt)) return;
                 const auto t0 = Clock::now();
                 bt->clear();
+                bt->want_device_ids = device_ids;
                 bt->reserve_ids(kBatchIds + kBatchIds / 4);
                 const bool got = reader.fill(*bt, max_docs, kBatchIds);
                 read_s += since(t0);
@@ -284,6 +292,8 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
                     job.indices = bt->ids;
                     job.n = bt->n;
                     job.pinned_input = true;
+                    if (bt->want_device_ids && bt->d_dev == devs[di] && bt->d_valid == bt->nids())
+                        job.d_indices = bt->d_ids;
                     inflight[bt->seq] = bt;
                     lane.submit(job, on_done);
                 }
