@@ -3,7 +3,8 @@ reference: identical sketch files for well-formed corpora in every spelling
 the fast grammar takes (labels +1/-1/1/0/+0/-0, tabs, CRLF, leading zeros,
 blank lines), for corpora mixing lines only the CPU parser takes (comments,
 "1.0" values, signed ids), across block sizes that split the corpus into many
-device blocks; and identical errors, line numbers included, when a bad line
+device blocks, with the parsed ids kept on the device or copied back; and
+identical errors, line numbers included, when a bad line
 sits deep inside a corpus."""
 import os
 
@@ -83,6 +84,13 @@ def test_gpu_parse_matches_cpu_and_reference(bb, ref, tmp_path, mixed):
         assert g == cpu, (mixed, block)
         if not mixed:
             assert launches > 4, "the GPU parser did not run"
+    # ids copied back to the host after parsing, instead of kept on the device
+    os.environ["BBMH_DEVICE_IDS"] = "0"
+    try:
+        (g, _) = _sketch(bb, str(path), str(tmp_path / "gpu2.bbmh"), gpu=True, block=1 << 16)
+    finally:
+        os.environ.pop("BBMH_DEVICE_IDS")
+    assert g == cpu, mixed
 
 
 @pytest.mark.parametrize("bad", ["3:2", "descending", "label", "idx0"])
