@@ -692,9 +692,11 @@ private:
         size_t cut2 = 0;
         bool eof2 = false;
         const bool full = !whole;
-        if (plan_block(full ? max_docs : max_docs - b.n, full ? max_ids : max_ids - std::min(max_ids, b.nids()),
-                       full || b.n == 0, pos_, cut2, eof2, false) == 1 &&
-            !gpu_->prefetched(file_pos(pos_), cut2 - pos_))
+        int plan2 = plan_block(full ? max_docs : max_docs - b.n, full ? max_ids : max_ids - std::min(max_ids, b.nids()),
+                               full || b.n == 0, pos_, cut2, eof2, false);
+        if (plan2 == 2)  // this batch takes no more: the block opens the next one
+            plan2 = plan_block(max_docs, max_ids, true, pos_, cut2, eof2, false);
+        if (plan2 == 1 && !gpu_->prefetched(file_pos(pos_), cut2 - pos_))
             gpu_->prefetch(buf_->data() + pos_, cut2 - pos_, file_pos(pos_));
         if (full) return 2;
         return pos_ < len_ || sealed_ || !eof_ || r.rows ? 1 : 0;
