@@ -241,9 +241,12 @@ def run_loader(tmp, n_docs):
     for path, kind in ((path_b, "bbcv"), (path_t, "libsvm")):
         size = os.path.getsize(path)
         f.sketch_file(path, os.path.join(tmp, "o.bbmh"), 8, 10000, threads)
-        t = time.perf_counter()
-        stats = f.sketch_file(path, os.path.join(tmp, "o.bbmh"), 8, 10000, threads)
-        wall = time.perf_counter() - t
+        wall, stats = 1e30, None
+        for _ in range(3):  # best of 3 (page cache warm)
+            t = time.perf_counter()
+            st = f.sketch_file(path, os.path.join(tmp, "o.bbmh"), 8, 10000, threads)
+            if time.perf_counter() - t < wall:
+                wall, stats = time.perf_counter() - t, st
         emit({"config": "loader", "format": kind, "docs": n_docs, "bytes": size, "wall_s": wall,
               "input_mb_per_s": size / wall / 1e6, "docs_per_s": n_docs / wall,
               "hash_evals_per_s": n_docs * bench.NNZ * 500 / wall, "stats": stats,
