@@ -31,8 +31,7 @@ namespace bbmh {
 
 namespace {
 
-constexpr uint32_t kTpb = 256;              // threads per CTA; one 16-byte chunk each
-constexpr uint32_t kCtaBytes = kTpb * 16;   // bytes per CTA ("segment")
+constexpr uint32_t kTpb = 256;  // threads per CTA, one 16-byte chunk each: a segment is kTpb * 16 bytes
 
 __device__ __forceinline__ bool is_sep(char c) { return c == ' ' || c == '\t'; }
 __device__ __forceinline__ bool is_ws_or_nl(char c) {
