@@ -23,6 +23,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
@@ -108,6 +109,8 @@ void read_exact(FILE* f, void* p, size_t n) {
 // page-locked buffer. The first failing record (lowest index) wins, with the
 // reference's messages (dataio.cpp:211-230).
 class BinaryReader : public CorpusReader {
+    std::atomic<uint32_t> sink_{0};
+
 public:
     BinaryReader(const std::string& path, unsigned threads)
         : path_(path), threads_(std::max(1u, std::min(threads, 64u))) {
@@ -146,6 +149,20 @@ public:
         if (fd_ >= 0) ::close(fd_);
     }
 
+    // Maps the pages of [off, off + n) on all pool threads. A batch's header
+    // walk otherwise takes one page fault per few records on one thread
+    // (~1.7 ms per 67 MB batch, as long as copying it).
+    void prefault(uint64_t off, uint64_t n) {
+        if (!map_ || n < (uint64_t(4) << 20)) return;
+        const unsigned T = std::min(16u, host_threads());
+        host_parallel(T, [&](unsigned w) {
+            const uint64_t lo = off + n * w / T, hi = off + n * (w + 1) / T;
+            uint32_t acc = 0;
+            for (uint64_t p = lo; p < hi; p += 4096) acc += map_[p];
+            sink_.fetch_add(acc, std::memory_order_relaxed);  // keep the reads
+        });
+    }
+
     bool fill(Batch& b, uint64_t max_docs, uint64_t max_ids) override {
         // 1. sequential header walk
         struct Rec {
@@ -159,6 +176,7 @@ public:
         bool pending = false;
         uint64_t nid = b.nids();
         const uint64_t first = read_;
+        prefault(pos_, std::min<uint64_t>(size_ - pos_, (max_ids + max_ids / 4) * 4 + 5 * max_docs));
         while (read_ < count_ && b.n + recs.size() < max_docs && (nid < max_ids || recs.empty())) {
             if (pos_ + 1 > size_) {
                 pending = true, pend_code = Errc::Io, pend_msg = "short read";
@@ -186,6 +204,7 @@ public:
             ++read_;
         }
         if (recs.empty() && !pending) return false;
+        trace("bbcv: headers walked");
         if (nid > b.cap_ids) b.reserve_ids(std::max<uint64_t>(nid, max_ids + max_ids / 4));
         // 2. parallel copy + strictly-ascending check
         const size_t nr = recs.size();
@@ -206,6 +225,7 @@ public:
             }
         };
         host_parallel(W, work);
+        trace("bbcv: ids copied");
         for (unsigned w = 0; w < W; ++w)
             if (bad[w] != UINT64_MAX)
                 fail(Errc::NonAscendingIndex, "record " + std::to_string(first + bad[w]));
