@@ -236,7 +236,10 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
                 const auto t0 = Clock::now();
                 bt->clear();
                 bt->want_device_ids = device_ids;
-                bt->reserve_ids(kBatchIds + kBatchIds / 4);
+                // (device-resident ids need host room only for rows the CPU
+                // parser takes, reserved on demand: 84 MB of page-locked memory
+                // per batch cost ~35 ms to allocate on a process's first call)
+                if (!device_ids) bt->reserve_ids(kBatchIds + kBatchIds / 4);
                 const bool got = reader.fill(*bt, max_docs, kBatchIds);
                 read_s += since(t0);
                 trace("reader: batch filled");
