@@ -427,7 +427,7 @@ public:
         gpu_ = res_->gpu.get();
         gpu_block_ = gpu_parse_block_bytes(kGpuBlock);
         // GPU mode: two windows, each with room for the block being parsed,
-        // the next one, the read-ahead block and a few more (4 blocks measured 7% slower)
+        // the next one, the read-ahead block and a few more (4 blocks: 7% slower; 8: no faster)
         // (a block size set through the test knob sizes the windows alone, so
         // small corpora exercise the window switch)
         const size_t win = gpu_block_ == kGpuBlock ? std::max(2 * kBlock, 6 * gpu_block_) : 6 * gpu_block_;
