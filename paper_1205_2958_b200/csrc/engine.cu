@@ -802,7 +802,10 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
             // With several (lanes here, or ranks of one job on this node,
             // LOCAL_WORLD_SIZE) they share the host's DRAM, and N links reading
             // 4 B per id beat encodes costing 8 B of DRAM traffic per id.
-            lane.set_delta16(devs.size() == 1 && local_gpu_processes() == 1);
+            // The encode runs ~4.5 GB/s of ids per host core (profiles/r11/
+            // host_encode_probe.jsonl); below ~12 cores it is slower than the
+            // link's 4-byte copy.
+            lane.set_delta16(devs.size() == 1 && local_gpu_processes() == 1 && host_threads() >= 12);
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
                 if (codes && res.codes != codes + r0 * cb) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);
