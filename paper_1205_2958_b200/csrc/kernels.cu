@@ -457,19 +457,25 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
         if (lane < head) eval(__ldg(ids + lane));
         const uint64_t nq = (nnz - head) / 4;
         const uint4* q4 = reinterpret_cast<const uint4*>(ids + head);
+        // two quads per lane per step, the next step's loaded under this one's
+        // hashing (with one step's loads in flight per warp the k = 8 launch
+        // reached 68% of HBM)
+        uint4 x = lane < nq ? __ldg(q4 + lane) : make_uint4(0, 0, 0, 0);
+        uint4 y = lane + 32 < nq ? __ldg(q4 + lane + 32) : x;
         for (uint64_t q = lane; q < nq; q += 64) {
-            const uint4 x = __ldg(q4 + q);
+            const uint4 cx = x, cy = y;
             const bool two = q + 32 < nq;
-            const uint4 y = two ? __ldg(q4 + q + 32) : x;
-            eval(x.x);
-            eval(x.y);
-            eval(x.z);
-            eval(x.w);
+            if (q + 64 < nq) x = __ldg(q4 + q + 64);
+            if (q + 96 < nq) y = __ldg(q4 + q + 96);
+            eval(cx.x);
+            eval(cx.y);
+            eval(cx.z);
+            eval(cx.w);
             if (two) {
-                eval(y.x);
-                eval(y.y);
-                eval(y.z);
-                eval(y.w);
+                eval(cy.x);
+                eval(cy.y);
+                eval(cy.z);
+                eval(cy.w);
             }
         }
         const uint64_t t0 = head + 4 * nq;
