@@ -530,7 +530,11 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
                 uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
                 uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
     auto kern = sketch_kernel<SCHEME, POW2, J>;
-    int tile = env_int("BBMH_TUNE_TILE", SCHEME == S_2U ? 1024 : (int)kDefaultTile);
+    // 1,024-id tiles for 2U and for 4U below 256 threads per CTA: 4U CTAs of one
+    // or two warps with 4,096-id tiles are held to ~7 per SM by shared memory
+    // (k = 32: 0.91 -> 1.25 T evals/s, k = 64: 0.95 -> 1.31; tools/grid_4u_tiles.json)
+    const bool small_tile = SCHEME == S_2U || ((SCHEME == S_4UBIT || SCHEME == S_4UMOD) && sh.tpb < 256);
+    int tile = env_int("BBMH_TUNE_TILE", small_tile ? 1024 : (int)kDefaultTile);
     tile = tile < 64 ? 64 : tile > 16384 ? 16384 : tile & ~3;
     const size_t smem = (2 * (tile + 8) + sh.jtile) * sizeof(uint32_t);
     int dev = 0;
