@@ -457,25 +457,29 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
         if (lane < head) eval(__ldg(ids + lane));
         const uint64_t nq = (nnz - head) / 4;
         const uint4* q4 = reinterpret_cast<const uint4*>(ids + head);
-        // two quads per lane per step, the next step's loaded under this one's
+        // kQ quads per lane per step, the next step's loaded under this one's
         // hashing (with one step's loads in flight per warp the k = 8 launch
         // reached 68% of HBM)
-        uint4 x = lane < nq ? __ldg(q4 + lane) : make_uint4(0, 0, 0, 0);
-        uint4 y = lane + 32 < nq ? __ldg(q4 + lane + 32) : x;
-        for (uint64_t q = lane; q < nq; q += 64) {
-            const uint4 cx = x, cy = y;
-            const bool two = q + 32 < nq;
-            if (q + 64 < nq) x = __ldg(q4 + q + 64);
-            if (q + 96 < nq) y = __ldg(q4 + q + 96);
-            eval(cx.x);
-            eval(cx.y);
-            eval(cx.z);
-            eval(cx.w);
-            if (two) {
-                eval(cy.x);
-                eval(cy.y);
-                eval(cy.z);
-                eval(cy.w);
+        constexpr int kQ = SCHEME == S_2U && J <= 8 ? 4 : 2;  // quads per lane per step
+        uint4 nx[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i)
+            nx[i] = lane + 32 * i < nq ? __ldg(q4 + lane + 32 * i) : make_uint4(0, 0, 0, 0);
+        for (uint64_t q = lane; q < nq; q += 32 * kQ) {
+            uint4 cx[kQ];
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) {
+                cx[i] = nx[i];
+                if (q + 32 * (kQ + i) < nq) nx[i] = __ldg(q4 + q + 32 * (kQ + i));
+            }
+#pragma unroll
+            for (int i = 0; i < kQ; ++i) {
+                if (i == 0 || q + 32 * i < nq) {
+                    eval(cx[i].x);
+                    eval(cx[i].y);
+                    eval(cx[i].z);
+                    eval(cx[i].w);
+                }
             }
         }
         const uint64_t t0 = head + 4 * nq;
