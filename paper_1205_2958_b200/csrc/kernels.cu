@@ -434,15 +434,36 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
     for (int r = 0; r < J; ++r) c[r].load(Fm, (uint32_t)r < k ? r : k - 1);
     const uint32_t mask = b >= 32 ? 0xffffffffu : ((1u << b) - 1);
     const uint64_t cb = ((uint64_t)k * b + 7) >> 3;
-    for (uint64_t doc = (uint64_t)blockIdx.x * W + warp; doc < n_docs;
-         doc += (uint64_t)gridDim.x * W) {
-        uint64_t beg = row_ptr[doc], end = row_ptr[doc + 1];
+    // kQ quads per lane per step, the next step's loaded under this one's
+    // hashing, and the next document's first step under this one's merge and
+    // epilogue (with one step's loads in flight per warp the k = 8 launch
+    // reached 68% of HBM)
+    constexpr int kQ = SCHEME == S_2U && J <= 8 ? 4 : 2;  // quads per lane per step
+    const uint64_t stride = (uint64_t)gridDim.x * W;
+    const uint32_t* ids = nullptr;
+    uint64_t nnz = 0, head = 0, nq = 0;
+    const uint4* q4 = nullptr;
+    uint4 nx[kQ];
+    auto describe = [&](uint64_t d) {  // document d's id ranges and first step
+        uint64_t beg = row_ptr[d], end = row_ptr[d + 1];
         if (end < beg) {
             if (lane == 0) atomicOr(err, 2);
             end = beg;
         }
-        const uint32_t* ids = indices + (beg - index_base);
-        const uint64_t nnz = end - beg;
+        ids = indices + (beg - index_base);
+        nnz = end - beg;
+        // head ids up to 16-byte alignment, whole quads, tail ids
+        const uint64_t h = ((16 - ((uintptr_t)ids & 15)) & 15) / 4;
+        head = nnz < h ? nnz : h;
+        nq = (nnz - head) / 4;
+        q4 = reinterpret_cast<const uint4*>(ids + head);
+#pragma unroll
+        for (int i = 0; i < kQ; ++i)
+            nx[i] = lane + 32 * i < nq ? __ldg(q4 + lane + 32 * i) : make_uint4(0, 0, 0, 0);
+    };
+    uint64_t doc = (uint64_t)blockIdx.x * W + warp;
+    if (doc < n_docs) describe(doc);
+    for (; doc < n_docs; doc += stride) {
         uint32_t m[J];
 #pragma unroll
         for (int r = 0; r < J; ++r) m[r] = 0xffffffffu;
@@ -451,20 +472,7 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
 #pragma unroll
             for (int r = 0; r < J; ++r) m[r] = min(m[r], hash1<SCHEME, POW2>(Fm, c[r], tt));
         };
-        // head ids up to 16-byte alignment, whole quads, tail ids
-        const uint64_t head = nnz < ((16 - ((uintptr_t)ids & 15)) & 15) / 4
-                                  ? nnz : ((16 - ((uintptr_t)ids & 15)) & 15) / 4;
         if (lane < head) eval(__ldg(ids + lane));
-        const uint64_t nq = (nnz - head) / 4;
-        const uint4* q4 = reinterpret_cast<const uint4*>(ids + head);
-        // kQ quads per lane per step, the next step's loaded under this one's
-        // hashing (with one step's loads in flight per warp the k = 8 launch
-        // reached 68% of HBM)
-        constexpr int kQ = SCHEME == S_2U && J <= 8 ? 4 : 2;  // quads per lane per step
-        uint4 nx[kQ];
-#pragma unroll
-        for (int i = 0; i < kQ; ++i)
-            nx[i] = lane + 32 * i < nq ? __ldg(q4 + lane + 32 * i) : make_uint4(0, 0, 0, 0);
         for (uint64_t q = lane; q < nq; q += 32 * kQ) {
             uint4 cx[kQ];
 #pragma unroll
@@ -484,6 +492,8 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
         }
         const uint64_t t0 = head + 4 * nq;
         if (t0 + lane < nnz) eval(__ldg(ids + t0 + lane));
+        const bool empty = nnz == 0;
+        if (doc + stride < n_docs) describe(doc + stride);  // loads in flight during the merge
         // merge the 32 lanes' minima, function by function
 #pragma unroll
         for (int r = 0; r < J; ++r) {
@@ -492,7 +502,6 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
                 m[r] = min(m[r], __shfl_xor_sync(0xffffffffu, m[r], off));
             if constexpr (SCHEME == S_2U) m[r] >>= Fm.shift2u;
         }
-        const bool empty = nnz == 0;
         if (lane == 0) {
 #pragma unroll
             for (int r = 0; r < J; ++r)
