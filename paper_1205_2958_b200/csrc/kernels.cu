@@ -613,7 +613,7 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
         case 4: return launch_one<SCHEME, POW2, 4>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         case 8: return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         case 7:
-            if constexpr (SCHEME == S_2U)
+            if constexpr (SCHEME != S_PERM)
                 return launch_one<SCHEME, POW2, 7>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         default: return launch_one<SCHEME, POW2, 16>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
@@ -674,13 +674,14 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     const double docs = n ? (double)n : 1e12;
     LaunchShape best;
     double best_cost = 1e300;
-    // J = 7 (2U only): 7 x 32 = 224 lanes fit k = 200 (config 1) with 11% idle
-    // instead of 22% at 256
+    // J = 7: 7 x 32 = 224 lanes fit k = 200 (config 1) with 11% idle instead of
+    // 22% at 256 (4U at k = 200: 1.02 -> 1.19 T evals/s against J = 1 x 224,
+    // tools/grid_4u_k200b.json)
     const int Js[5] = {8, 7, 4, 2, 1};
     for (int J : Js) {
-        if (J == 7 && scheme != S_2U) continue;
+        if (J == 7 && scheme == S_PERM) continue;
         const double eff = scheme == S_2U ? (J == 8 ? 1.0 : J == 7 ? 1.02 : J == 4 ? 1.06 : J == 2 ? 1.1 : 1.35)
-                                          : (J == 2 ? 1.0 : J == 4 ? 1.01 : J == 8 ? 1.02 : 1.02);
+                                          : (J == 2 || J == 7 ? 1.0 : J == 4 ? 1.01 : J == 8 ? 1.02 : 1.02);
         for (int tpb = 32; tpb <= 256; tpb += 32) {
             const uint64_t jtile = (uint64_t)tpb * J;
             const uint64_t tiles = (k + jtile - 1) / jtile;
@@ -699,7 +700,7 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     }
     // developer tuning knobs (not part of the ABI)
     const int J = env_int("BBMH_TUNE_J", 0), tpb = env_int("BBMH_TUNE_TPB", 0);
-    if ((J == 1 || J == 2 || J == 4 || J == 8 || (J == 7 && scheme == S_2U)) && tpb >= 32 &&
+    if ((J == 1 || J == 2 || J == 4 || J == 8 || (J == 7 && scheme != S_PERM)) && tpb >= 32 &&
         tpb <= 256 && tpb % 32 == 0) {
         best.J = J;
         best.tpb = tpb;
