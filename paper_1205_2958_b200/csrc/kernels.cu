@@ -616,6 +616,14 @@ void dispatch_j(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
             if constexpr (SCHEME != S_PERM)
                 return launch_one<SCHEME, POW2, 7>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case 5:
+            if constexpr (SCHEME == S_2U)
+                return launch_one<SCHEME, POW2, 5>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case 6:
+            if constexpr (SCHEME == S_2U)
+                return launch_one<SCHEME, POW2, 6>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            return launch_one<SCHEME, POW2, 8>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         default: return launch_one<SCHEME, POW2, 16>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
     }
 }
@@ -677,10 +685,16 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     // J = 7: 7 x 32 = 224 lanes fit k = 200 (config 1) with 11% idle instead of
     // 22% at 256 (4U at k = 200: 1.02 -> 1.19 T evals/s against J = 1 x 224,
     // tools/grid_4u_k200b.json)
-    const int Js[5] = {8, 7, 4, 2, 1};
+    // J = 5, 6 (2U): 5 x 64 = 320 lanes fit k = 300 (9.2 -> 12.8 T evals/s), and
+    // 5 x 32 = 160 fit k = 160 (9.0 -> 12.9; tools/grid_2u_k300.json). The 2U
+    // costs of thin J are measured (k = 64 with J = 2: 1.28; k = 300 with J = 2
+    // x 160 threads: ~1.5).
+    const int Js[7] = {8, 7, 6, 5, 4, 2, 1};
     for (int J : Js) {
         if (J == 7 && scheme == S_PERM) continue;
-        const double eff = scheme == S_2U ? (J == 8 ? 1.0 : J == 7 ? 1.02 : J == 4 ? 1.06 : J == 2 ? 1.1 : 1.35)
+        if ((J == 5 || J == 6) && scheme != S_2U) continue;
+        const double eff = scheme == S_2U ? (J == 8 ? 1.0 : J == 7 ? 1.02 : J == 6 ? 1.03 : J == 5 ? 1.08
+                                             : J == 4 ? 1.10 : J == 2 ? 1.3 : 1.35)
                                           : (J == 2 || J == 7 ? 1.0 : J == 4 ? 1.01 : J == 8 ? 1.02 : 1.02);
         for (int tpb = 32; tpb <= 256; tpb += 32) {
             const uint64_t jtile = (uint64_t)tpb * J;
@@ -700,7 +714,8 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     }
     // developer tuning knobs (not part of the ABI)
     const int J = env_int("BBMH_TUNE_J", 0), tpb = env_int("BBMH_TUNE_TPB", 0);
-    if ((J == 1 || J == 2 || J == 4 || J == 8 || (J == 7 && scheme != S_PERM)) && tpb >= 32 &&
+    if ((J == 1 || J == 2 || J == 4 || J == 8 || (J == 7 && scheme != S_PERM) ||
+         ((J == 5 || J == 6) && scheme == S_2U)) && tpb >= 32 &&
         tpb <= 256 && tpb % 32 == 0) {
         best.J = J;
         best.tpb = tpb;
