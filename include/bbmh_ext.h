@@ -112,6 +112,27 @@ BBMH_API void bbmh_ext_transfer_bytes(uint64_t* h2d_out, uint64_t* d2h_out);
  * 0 restores the default. */
 BBMH_API bbmh_status bbmh_ext_set_chunk_docs(uint64_t docs);
 
+/* Tuning and test switches (the reference has none and reads no environment,
+ * SPEC.md:502). Every switch defaults to what the product runs; names and
+ * meanings are listed in csrc/options.hpp, in order by bbmh_ext_option_name
+ * (returns "" past the end). For developer A/B runs BBMH_OPT_<NAME> in the
+ * environment sets a start value, read once. Unknown names fail with
+ * BBMH_E_INVALID_ARGUMENT. */
+BBMH_API bbmh_status bbmh_ext_set_option(const char* name, int64_t value);
+BBMH_API bbmh_status bbmh_ext_get_option(const char* name, int64_t* value_out);
+BBMH_API const char* bbmh_ext_option_name(uint32_t i);
+
+/* Monotonic per-process counters of which routes ran: "kernel_launches",
+ * "h2d_bytes", "d2h_bytes", "peer_copy_bytes", "zero_copy_calls",
+ * "delta16_chunks", "raw_chunks", "range_shards", "device_id_batches". */
+BBMH_API bbmh_status bbmh_ext_counter(const char* name, uint64_t* value_out);
+
+/* Permutation table j (dim u32 values, the reference's perm_[j*D .. j*D+D),
+ * hash_family.hpp:88-89) copied into table_out, wherever the family keeps it
+ * (host build or the GPU that built it). */
+BBMH_API bbmh_status bbmh_ext_family_perm_table(const bbmh_family* family, uint32_t j,
+                                                uint32_t* table_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,6 +100,11 @@ def lib() -> C.CDLL:
         "bbmh_ext_kernel_launches": ([], C.c_uint64),
         "bbmh_ext_transfer_bytes": ([u64p, u64p], None),
         "bbmh_ext_set_chunk_docs": ([C.c_uint64], C.c_int32),
+        "bbmh_ext_set_option": ([C.c_char_p, C.c_int64], C.c_int32),
+        "bbmh_ext_get_option": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int32),
+        "bbmh_ext_option_name": ([C.c_uint32], C.c_char_p),
+        "bbmh_ext_counter": ([C.c_char_p, u64p], C.c_int32),
+        "bbmh_ext_family_perm_table": ([C.c_void_p, C.c_uint32, u32p], C.c_int32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -177,6 +182,12 @@ class Family:
     def prepare(self, device: int = 0):
         _check(lib().bbmh_ext_family_prepare(self.handle, device))
 
+    def perm_table(self, j: int) -> np.ndarray:
+        """bbmh_ext_family_perm_table: permutation table j (u32[dim])."""
+        out = np.empty(self.dim, np.uint32)
+        _check(lib().bbmh_ext_family_perm_table(self.handle, j, _ptr(out, u32p)))
+        return out
+
     # ---- sketching ------------------------------------------------------
     def sketch_set(self, indices, b: int, want_minima: bool = True):
         """bbmh_sketch_set: -> (codes u8[ceil(k*b/8)], minima u64[k] | None, empty)."""
@@ -197,7 +208,14 @@ class Family:
         idx = np.ascontiguousarray(indices, dtype=np.uint32)
         n = rp.size - 1
         cb = code_bytes(self.k, b)
-        codes = codes_out if codes_out is not None else np.empty(n * cb, np.uint8)
+        if codes_out is not None:
+            # the library writes n*cb bytes through this pointer
+            if (not isinstance(codes_out, np.ndarray) or codes_out.dtype != np.uint8
+                    or not codes_out.flags.c_contiguous or codes_out.size < n * cb):
+                raise ValueError(f"codes_out must be a C-contiguous uint8 array of >= {n * cb} bytes")
+            codes = codes_out[: n * cb]
+        else:
+            codes = np.empty(n * cb, np.uint8)
         minima = np.empty(n * self.k, np.uint64) if want_minima else None
         flags = np.empty(n, np.uint8)
         _check(lib().bbmh_ext_sketch_csr(self.handle, _ptr(rp, u64p),
@@ -272,6 +290,53 @@ def get_devices() -> list:
 
 def set_chunk_docs(docs: int) -> None:
     _check(lib().bbmh_ext_set_chunk_docs(docs))
+
+
+def set_option(name: str, value: int) -> None:
+    """bbmh_ext_set_option (tuning and test switches, csrc/options.hpp)."""
+    _check(lib().bbmh_ext_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = C.c_int64(0)
+    _check(lib().bbmh_ext_get_option(name.encode(), C.byref(v)))
+    return v.value
+
+
+def option_names() -> list:
+    out, i = [], 0
+    while True:
+        nm = lib().bbmh_ext_option_name(i).decode()
+        if not nm:
+            return out
+        out.append(nm)
+        i += 1
+
+
+class option:
+    """Context manager: set options for a block, restore them after.
+        with bbmh.option(delta16=1, chunk_ids=1 << 20): ..."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            set_option(k, v)
+
+
+def counter(name: str) -> int:
+    """bbmh_ext_counter: monotonic count of a route taken (see bbmh_ext.h)."""
+    v = C.c_uint64(0)
+    _check(lib().bbmh_ext_counter(name.encode(), C.byref(v)))
+    return v.value
 
 
 def kernel_launches() -> int:

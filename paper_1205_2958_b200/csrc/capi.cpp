@@ -15,6 +15,7 @@
 #include "core.hpp"
 #include "engine.hpp"
 #include "estimate.hpp"
+#include "options.hpp"
 #include "pipeline.hpp"
 
 using namespace bbmh;
@@ -303,6 +304,41 @@ void bbmh_ext_transfer_bytes(uint64_t* h2d_out, uint64_t* d2h_out) {
 
 bbmh_status bbmh_ext_set_chunk_docs(uint64_t docs) {
     return guarded([&] { set_chunk_docs(docs); });
+}
+
+bbmh_status bbmh_ext_set_option(const char* name, int64_t value) {
+    return guarded([&] {
+        require(name, "name");
+        if (!set_opt(name, value)) fail(Errc::InvalidArgument, std::string("unknown option ") + name);
+    });
+}
+
+bbmh_status bbmh_ext_get_option(const char* name, int64_t* value_out) {
+    return guarded([&] {
+        require(name, "name");
+        if (!value_out) fail(Errc::InvalidArgument, "value_out must not be NULL");
+        if (!get_opt(name, value_out)) fail(Errc::InvalidArgument, std::string("unknown option ") + name);
+    });
+}
+
+const char* bbmh_ext_option_name(uint32_t i) { return opt_name(int(i)); }
+
+bbmh_status bbmh_ext_counter(const char* name, uint64_t* value_out) {
+    return guarded([&] {
+        require(name, "name");
+        if (!value_out) fail(Errc::InvalidArgument, "value_out must not be NULL");
+        if (!counter_value(name, value_out)) fail(Errc::InvalidArgument, std::string("unknown counter ") + name);
+    });
+}
+
+bbmh_status bbmh_ext_family_perm_table(const bbmh_family* family, uint32_t j, uint32_t* table_out) {
+    return guarded([&] {
+        if (!family) fail(Errc::InvalidArgument, "family must not be NULL");
+        if (!table_out) fail(Errc::InvalidArgument, "table_out must not be NULL");
+        const Family& f = *family->impl;
+        if (f.scheme != Scheme::Permutation) fail(Errc::InvalidArgument, "not a permutation family");
+        copy_perm_table(f, j, table_out);
+    });
 }
 
 // ---- resemblance estimation (capi.cpp:187-240) ---------------

@@ -46,7 +46,7 @@ private:
 
 [[noreturn]] inline void fail(Errc code, std::string msg) { throw Error(code, std::move(msg)); }
 
-// Developer tracing: with BBMH_TRACE=1 in the environment, prints
+// Developer tracing: with the "trace" option on (options.hpp), prints
 // "bbmh-trace <ms since first call> <what>" to stderr (pipeline stage timing).
 void trace(const char* what);
 bool trace_on();

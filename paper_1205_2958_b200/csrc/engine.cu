@@ -18,6 +18,7 @@
 #include "engine.hpp"
 #include "delta.hpp"
 #include "hostpool.hpp"
+#include "options.hpp"
 
 namespace bbmh {
 
@@ -195,6 +196,7 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device,
                 cudaGetLastError();
             }
             BBMH_CUDA(cudaMemcpyPeer(df->d_perm, device, f.perm_dev, f.perm_dev_id, bytes));
+            count_peer_copy(bytes);
         } else {
             BBMH_CUDA(cudaMalloc(&df->d_perm, bytes));
             upload_large(df->d_perm, f.perm.data(), bytes);
@@ -289,9 +291,29 @@ void check_row_ptr(const uint64_t* rp, uint64_t n) {
 void adopt_device_perm(Family& f, int device, uint32_t* d_perm) {
     std::lock_guard lk(f.dev_mu);
     if (size_t(device) >= f.dev.size()) f.dev.resize(device + 1);
-    f.dev[device] = upload_family(f, device, d_perm);
     f.perm_dev = d_perm;
     f.perm_dev_id = device;
+    if (opt(Opt::ForcePeerCopy)) {
+        // test hook: replicate through the peer-copy branch other GPUs take
+        // (a same-device cudaMemcpyPeer), then serve from the replica
+        f.dev[device] = upload_family(f, device);
+        DeviceGuard g(device);
+        BBMH_CUDA(cudaFree(d_perm));
+        f.perm_dev = f.dev[device]->d_perm;
+        return;
+    }
+    f.dev[device] = upload_family(f, device, d_perm);
+}
+
+void copy_perm_table(const Family& f, uint32_t j, uint32_t* out) {
+    if (j >= f.k) fail(Errc::InvalidArgument, "j must be < k");
+    if (!f.perm.empty()) {
+        std::memcpy(out, f.perm.data() + size_t(j) * f.dim, size_t(f.dim) * sizeof(uint32_t));
+        return;
+    }
+    DeviceGuard g(f.perm_dev_id);
+    BBMH_CUDA(cudaMemcpy(out, f.perm_dev + size_t(j) * f.dim, size_t(f.dim) * sizeof(uint32_t),
+                         cudaMemcpyDeviceToHost));
 }
 
 uint32_t perm_value_on_device(const Family& f, uint32_t j, uint32_t t) {
@@ -443,11 +465,11 @@ void d2h(void* h, const void* d, size_t n, cudaStream_t st) {
 // and decode_delta16 rebuilds them in the slot's id buffer before the sketch.
 namespace {
 
-// BBMH_DELTA_H2D: 0 off, 1 on whenever possible (tests), unset: where it
+// option "delta16": 0 off, 1 on whenever possible (tests), -1: where it
 // pays, on lanes that allow it (Lane::set_delta16)
 int delta16_mode() {
-    const char* e = std::getenv("BBMH_DELTA_H2D");  // read per chunk: tests flip it
-    return e && *e ? (*e == '0' ? 0 : 1) : 2;
+    const int64_t v = opt(Opt::Delta16);
+    return v < 0 ? 2 : v == 0 ? 0 : 1;
 }
 
 // The H2D of 4 B per id bounds the chunk when the kernel's time per id is
@@ -465,17 +487,35 @@ bool delta16_pays(const KernelFamily& kf) {
 constexpr uint64_t kDeltaMinIds = 1ull << 21;
 
 uint64_t chunk_idx_cap() {
-    const char* e = std::getenv("BBMH_CHUNK_IDS");  // developer knob (A/B timing)
-    const uint64_t v = e && *e ? std::strtoull(e, nullptr, 10) : 0;
-    return v >= (1u << 16) ? v : kChunkIdxCap;
+    const int64_t v = opt(Opt::ChunkIds);
+    return v >= (1 << 16) ? uint64_t(v) : kChunkIdxCap;
 }
 
-// processes of this job on this node (torchrun / SLURM-style launchers set it)
-uint64_t local_gpu_processes() {
-    const char* e = std::getenv("LOCAL_WORLD_SIZE");
-    const long v = e ? std::atol(e) : 1;
-    return v > 1 ? uint64_t(v) : 1;
+// Host-encode rate of the 16-bit transfer, ids/s per host core (AVX2 encode
+// with streaming stores, profiles/r11/host_encode_probe.jsonl: ~4.5 GB/s of ids).
+constexpr double kEncodeIdsPerCore = 1.1e9;
+
+}  // namespace
+
+// Host bandwidth budget of the id transfer when `feeds` GPUs stream ids from
+// this host at once (lanes of this process x "host_sharers", e.g. the ranks
+// of one node). Per id, 4-byte ids cost 4 B of link and 4 B of DRAM reads
+// (the DMA); 2-byte ids cost 2 B of link, 8 B of DRAM traffic (the encode
+// reads 4 and writes 2, the DMA reads 2) and host-core time. The encode pays
+// when it moves more ids per second than the raw copy.
+bool delta16_budget_pays(uint64_t feeds, double* raw_ids_s, double* enc_ids_s) {
+    feeds = std::max<uint64_t>(1, feeds);
+    const double link = double(std::max<int64_t>(1, opt(Opt::PcieGbs))) * 1e9;
+    const double dram = host_dram_bytes_per_s();
+    const double cores = double(host_threads()) / double(feeds);  // cores per feed
+    const double raw = std::min(double(feeds) * link / 4, dram / 4);
+    const double enc = std::min({double(feeds) * link / 2, dram / 8, double(feeds) * cores * kEncodeIdsPerCore});
+    if (raw_ids_s) *raw_ids_s = raw;
+    if (enc_ids_s) *enc_ids_s = enc;
+    return enc > 1.05 * raw;
 }
+
+namespace {
 
 }  // namespace
 
@@ -513,6 +553,10 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
                                reinterpret_cast<uint32_t*>(h + d_exc_ptr),
                                reinterpret_cast<uint32_t*>(h + d_exc), exc_cap, nexc);
     if (delta) trace("lane: ids encoded");
+    count(delta ? Counter::Delta16Chunks : Counter::RawChunks);
+    // from here on the slot's stream may hold work: the slot must be drained
+    // before it is reused or returned, even if queueing below fails
+    s.busy = true;
     s.off_ids = delta ? d_deltas : align16((n + 1) * sizeof(uint64_t));
     s.off_err = delta ? align16(d_exc + nexc * sizeof(uint32_t)) : raw_err;
     s.off_scores = s.off_err + 16;
@@ -591,6 +635,8 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
     }
     s.packed = false;
     reserve(s, n, job.d_indices ? 0 : nidx, stage && !job.d_indices);
+    count(Counter::RawChunks);
+    s.busy = true;  // (see enqueue_packed)
     // row_ptr always goes through the slot's pinned mirror (small)
     std::memcpy(s.h_rp, job.row_ptr, (n + 1) * sizeof(uint64_t));
     h2d(s.d_rp, s.h_rp, (n + 1) * sizeof(uint64_t), s.st);
@@ -732,6 +778,7 @@ bool sketch_rows_zero_copy(const Family& f, int dev, const uint64_t* row_ptr,
     BBMH_CUDA(cudaGetLastError());
     BBMH_CUDA(cudaStreamSynchronize(s->st));
     count_transfer((n + 1) * sizeof(uint64_t) + (row_ptr[n] - row_ptr[0]) * sizeof(uint32_t), n + n * cb);
+    count(Counter::ZeroCopyCalls);
     if (codes) std::memcpy(codes, h + off_codes, n * cb);
     if (flags) std::memcpy(flags, h + off_flags, n);
     return true;
@@ -747,14 +794,12 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     check_row_ptr(row_ptr, n);
     const size_t cb = packed_code_bytes(f.k, b);
     const bool pinned = is_pinned(indices);
-    static const bool zero_copy_on = [] {
-        const char* e = std::getenv("BBMH_ZERO_COPY");  // developer knob (A/B timing)
-        return !(e && *e == '0');
-    }();
     // (zero-copy reads the caller's buffer in whole 16-byte granules: only
-    // when the last id ends one, so nothing past the caller's data is touched)
-    if (zero_copy_on && pinned && !minima && !score && f.scheme == Scheme::TwoU &&
+    // when the first id starts one and the last id ends one, so nothing
+    // outside the caller's data is touched)
+    if (opt(Opt::ZeroCopy) && pinned && !minima && !score && f.scheme == Scheme::TwoU &&
         row_ptr[n] - row_ptr[0] <= kZeroCopyMaxIds &&
+        ((uintptr_t)(indices + row_ptr[0]) & 15) == 0 &&
         ((uintptr_t)(indices + row_ptr[n]) & 15) == 0) {
         const std::vector<int> devs = pipeline_devices();
         if (devs.size() == 1 && sketch_rows_zero_copy(f, devs[0], row_ptr, indices, n, b, codes, flags))
@@ -765,10 +810,7 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     // and 2 B of PCIe, raw ones 4 B of each. With the encode bound by host
     // DRAM and the link idle half the time, sending some chunks raw moves
     // more ids per second than either alone.
-    const uint64_t raw_every = [] {
-        const char* e = std::getenv("BBMH_DELTA_RAW_EVERY");  // developer knob (A/B timing)
-        return e && *e ? std::strtoull(e, nullptr, 10) : uint64_t(0);
-    }();
+    const uint64_t raw_every = uint64_t(std::max<int64_t>(0, opt(Opt::DeltaRawEvery)));
     // a page-locked output buffer takes the codes' D2H directly
     const bool codes_pinned = codes && !minima && is_pinned(codes) && is_pinned(codes + n * cb - 1);
     // chunk boundaries: <= chunk_docs rows, <= kChunkIdxCap ids (unless one row is larger)
@@ -798,14 +840,11 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
         try {
             Lane lane(f, dev, b, minima != nullptr, score);
             lane.set_timed(false);
-            // one GPU feeding from this host: its cores are free to encode.
-            // With several (lanes here, or ranks of one job on this node,
-            // LOCAL_WORLD_SIZE) they share the host's DRAM, and N links reading
-            // 4 B per id beat encodes costing 8 B of DRAM traffic per id.
-            // The encode runs ~4.5 GB/s of ids per host core (profiles/r11/
-            // host_encode_probe.jsonl); below ~12 cores it is slower than the
-            // link's 4-byte copy.
-            lane.set_delta16(devs.size() == 1 && local_gpu_processes() == 1 && host_threads() >= 12);
+            // GPUs fed from this host (lanes here times the processes of the
+            // job that share it) split its DRAM and cores: the 16-bit transfer
+            // is used only where that budget says it moves ids faster.
+            lane.set_delta16(delta16_budget_pays(devs.size() * uint64_t(std::max<int64_t>(1, opt(Opt::HostSharers))),
+                                                 nullptr, nullptr));
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
                 if (codes && res.codes != codes + r0 * cb) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);

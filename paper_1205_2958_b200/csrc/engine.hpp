@@ -31,6 +31,14 @@ const DeviceFamily& device_family(const Family& f, int device);
 // (ownership passes to that device's DeviceFamily).
 void adopt_device_perm(Family& f, int device, uint32_t* d_perm);
 
+// Table j of a permutation family (D u32) into host memory, from wherever it
+// lives (the host build or the device that built it).
+void copy_perm_table(const Family& f, uint32_t j, uint32_t* out);
+
+// Whether 16-bit id transfer moves more ids/s than 4-byte ids when `feeds`
+// GPUs stream from this host (engine.cu); the two rates are returned too.
+bool delta16_budget_pays(uint64_t feeds, double* raw_ids_s, double* enc_ids_s);
+
 // Devices used by the host-buffer and file pipelines (empty = current device).
 std::vector<int> pipeline_devices();
 void set_pipeline_devices(const std::vector<int>& ids);

@@ -17,15 +17,12 @@
 #include <thread>
 
 #include "core.hpp"
+#include "options.hpp"
 
 namespace bbmh {
 
 bool trace_on() {
-    static const bool on = [] {
-        const char* e = std::getenv("BBMH_TRACE");
-        return e && *e && *e != '0';
-    }();
-    return on;
+    return opt(Opt::Trace) != 0;
 }
 
 void trace(const char* what) {

@@ -1,8 +1,11 @@
 // hostpool.cpp -- see hostpool.hpp.
 #include "hostpool.hpp"
+#include "options.hpp"
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <exception>
@@ -145,6 +148,36 @@ void host_memcpy(void* dst, const void* src, size_t n) {
         const size_t lo = n * w / T, hi = n * (w + 1) / T;
         std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
     });
+}
+
+double host_dram_bytes_per_s() {
+    if (const int64_t g = opt(Opt::HostDramGbs); g > 0) return double(g) * 1e9;
+    static const double measured = [] {
+        constexpr size_t kBytes = size_t(256) << 20;  // well past any host L3
+        char* a = static_cast<char*>(std::malloc(kBytes));
+        char* b = static_cast<char*>(std::malloc(kBytes));
+        if (!a || !b) {
+            std::free(a);
+            std::free(b);
+            return 100e9;
+        }
+        host_parallel(host_threads(), [&](unsigned w) {  // fault the pages in on every core
+            const size_t T = host_threads(), lo = kBytes * w / T, hi = kBytes * (w + 1) / T;
+            std::memset(a + lo, 1, hi - lo);
+            std::memset(b + lo, 0, hi - lo);
+        });
+        double best = 0;
+        for (int rep = 0; rep < 3; ++rep) {
+            const auto t0 = std::chrono::steady_clock::now();
+            host_memcpy(b, a, kBytes);
+            const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            best = std::max(best, 2.0 * double(kBytes) / s);
+        }
+        std::free(a);
+        std::free(b);
+        return best;
+    }();
+    return measured;
 }
 
 }  // namespace bbmh

@@ -17,6 +17,11 @@ unsigned host_threads();
 // first exception thrown by a task is rethrown here.
 void host_parallel(unsigned tasks, const std::function<void(unsigned)>& fn);
 
+// Host DRAM copy bandwidth (read + write bytes/s) of host_memcpy over the
+// whole pool, measured once per process on first use (~0.2 s: 2 x 256 MiB),
+// unless the "host_dram_gbs" option gives it.
+double host_dram_bytes_per_s();
+
 // memcpy split over the pool in pieces of >= 256 KiB (one thread copies ~10 GB/s).
 void host_memcpy(void* dst, const void* src, size_t n);
 

@@ -16,6 +16,7 @@
 #include "io.hpp"
 #include "parse.hpp"
 #include "hostpool.hpp"
+#include "options.hpp"
 
 #include <cuda_runtime.h>
 #include <fcntl.h>
@@ -786,11 +787,8 @@ private:
     // (one thread copies ~10 GB/s out of the page cache); returns bytes read.
     size_t read_at(char* p, size_t n) {
         const int fd = fileno(f_);
-        static const unsigned kReadThreads = [] {
-            const char* e = std::getenv("BBMH_READ_THREADS");  // developer knob (A/B timing)
-            const int v = e && *e ? std::atoi(e) : 0;
-            return v > 0 ? unsigned(v) : 16u;  // 8 -> 16 threads: 15.7 -> 17.5 GB/s of text
-        }();
+        // 8 -> 16 threads: 15.7 -> 17.5 GB/s of text
+        const unsigned kReadThreads = unsigned(std::max<int64_t>(1, opt(Opt::ReadThreads)));
         const unsigned T = n >= (size_t(16) << 20) ? std::min(kReadThreads, threads_) : 1u;
         std::vector<size_t> got(T, 0);
         std::vector<int> err(T, 0);

@@ -26,12 +26,14 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <string>
 #include <tuple>
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "options.hpp"
 
 namespace bbmh {
 
@@ -533,11 +535,6 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
     }
 }
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? std::atoi(v) : dflt;
-}
-
 template <int SCHEME, bool POW2, int J>
 void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* row_ptr,
                 uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
@@ -547,7 +544,8 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     // or two warps with 4,096-id tiles are held to ~7 per SM by shared memory
     // (k = 32: 0.91 -> 1.25 T evals/s, k = 64: 0.95 -> 1.31; tools/grid_4u_tiles.json)
     const bool small_tile = SCHEME == S_2U || ((SCHEME == S_4UBIT || SCHEME == S_4UMOD) && sh.tpb < 256);
-    int tile = env_int("BBMH_TUNE_TILE", small_tile ? 1024 : (int)kDefaultTile);
+    int tile = (int)opt(Opt::Tile);
+    if (tile <= 0) tile = small_tile ? 1024 : (int)kDefaultTile;
     tile = tile < 64 ? 64 : tile > 16384 ? 16384 : tile & ~3;
     const size_t smem = (2 * (tile + 8) + sh.jtile) * sizeof(uint32_t);
     int dev = 0;
@@ -555,11 +553,12 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     // occupancy/attribute queries cost several microseconds each: do them once
     // per (kernel instance, device, block shape, smem)
     static std::mutex mu;
-    static std::map<std::tuple<int, int, size_t>, std::pair<int, int>> cache;  // -> (sms, occ)
+    static std::map<std::tuple<int, int, size_t, int>, std::pair<int, int>> cache;  // -> (sms, occ)
     int sms = 148, occ = 1;
+    const int carveout = (int)opt(Opt::Carveout);
     {
         std::lock_guard lk(mu);
-        auto key = std::make_tuple(dev, sh.tpb, smem);
+        auto key = std::make_tuple(dev, sh.tpb, smem, carveout);
         auto it = cache.find(key);
         if (it == cache.end()) {
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -574,6 +573,12 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
             const int dyn_max = optin - (int)fa.sharedSizeBytes;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  dyn_max > (int)smem ? dyn_max : (int)smem);
+            // The persistent grid is sized to the occupancy limit, so the
+            // shared-memory carveout the driver picks at launch must admit
+            // that many CTAs; -1 leaves the choice to the driver.
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 carveout >= 0 && carveout <= 100 ? carveout : -1);
+            cudaGetLastError();
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sh.tpb, smem);
             occ = occ < 1 ? 1 : occ;
             it = cache.emplace(key, std::make_pair(sms, occ)).first;
@@ -585,10 +590,10 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     // run 8% faster at 20 CTAs per SM than at the 24 shared memory allows;
     // the thin-J ones (k <= 128) run 8% slower with that cap
     // (tools/grid_2u_cap.json, profiles/r11/ksweep_cap.txt).
-    if (SCHEME == S_2U && J >= 7 && sh.tpb == 32 && env_int("BBMH_TUNE_SMEM_CAP", 1))
+    if (SCHEME == S_2U && J >= 7 && sh.tpb == 32 && opt(Opt::SmemCap))
         occ = std::min(occ, 20);
-    const int ctas_env = env_int("BBMH_TUNE_CTAS_PER_SM", 0);
-    if (ctas_env > 0 && ctas_env < occ) occ = ctas_env;
+    const int ctas_cap = (int)opt(Opt::CtasPerSm);
+    if (ctas_cap > 0 && ctas_cap < occ) occ = ctas_cap;
     // persistent: one wave of CTAs per j-tile, each looping over documents
     uint64_t gx = (uint64_t)sms * occ / sh.jtiles;
     if (gx < 1) gx = 1;
@@ -712,8 +717,8 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
             }
         }
     }
-    // developer tuning knobs (not part of the ABI)
-    const int J = env_int("BBMH_TUNE_J", 0), tpb = env_int("BBMH_TUNE_TPB", 0);
+    // tuning switches (bbmh_ext_set_option "shape_j" / "shape_tpb")
+    const int J = (int)opt(Opt::ShapeJ), tpb = (int)opt(Opt::ShapeTpb);
     if ((J == 1 || J == 2 || J == 4 || J == 8 || (J == 7 && scheme != S_PERM) ||
          ((J == 5 || J == 6) && scheme == S_2U)) && tpb >= 32 &&
         tpb <= 256 && tpb % 32 == 0) {
@@ -730,7 +735,7 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
                    uint8_t* flags, int* err, cudaStream_t st) {
     if (n == 0) return;
     const uint32_t split_max = F.scheme == S_2U ? 32u : 16u;  // functions a lane holds in registers
-    if (F.k <= split_max && F.scheme != S_PERM && env_int("BBMH_SPLIT_SMALL_K", 1)) {
+    if (F.k <= split_max && F.scheme != S_PERM && opt(Opt::SplitSmallK)) {
         switch (F.scheme) {
             case S_2U: return dispatch_split<S_2U, true>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             case S_4UBIT:
@@ -756,9 +761,10 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
                 return dispatch_j<S_4UMOD, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             return dispatch_j<S_4UMOD, false>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         default:
-            if (perm_tablewise_applies(F, n))  // L2-resident table-outer schedule (perm.cu)
-                return launch_perm_tablewise(F, row_ptr, base, idx, n, b, codes, minima, flags,
-                                             err, st);
+            // L2-resident table-outer schedule (perm.cu)
+            if (perm_tablewise_applies(F, n) &&
+                launch_perm_tablewise(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st))
+                return;
             return dispatch_j<S_PERM, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
     }
 }
@@ -779,6 +785,35 @@ void count_transfer(uint64_t h2d, uint64_t d2h) {
 void transfer_counts(uint64_t& h2d, uint64_t& d2h) {
     h2d = g_h2d.load();
     d2h = g_d2h.load();
+}
+
+namespace {
+std::atomic<uint64_t> g_counters[int(Counter::kCount)];
+constexpr const char* kCounterNames[] = {"peer_copy_bytes", "zero_copy_calls", "delta16_chunks",
+                                         "raw_chunks", "range_shards", "device_id_batches"};
+static_assert(sizeof(kCounterNames) / sizeof(kCounterNames[0]) == size_t(Counter::kCount));
+}  // namespace
+
+void count(Counter c, uint64_t n) { g_counters[int(c)].fetch_add(n, std::memory_order_relaxed); }
+
+bool counter_value(const char* name, uint64_t* out) {
+    if (!name) return false;
+    const std::string s = name;
+    uint64_t v = 0;
+    if (s == "kernel_launches") {
+        v = g_launches.load();
+    } else if (s == "h2d_bytes") {
+        v = g_h2d.load();
+    } else if (s == "d2h_bytes") {
+        v = g_d2h.load();
+    } else {
+        int i = 0;
+        while (i < int(Counter::kCount) && s != kCounterNames[i]) ++i;
+        if (i == int(Counter::kCount)) return false;
+        v = g_counters[i].load();
+    }
+    if (out) *out = v;
+    return true;
 }
 
 }  // namespace bbmh

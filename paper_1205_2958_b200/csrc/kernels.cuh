@@ -48,7 +48,8 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t inde
 
 // Permutation mode with tables too large for L2: table-outer passes (perm.cu).
 bool perm_tablewise_applies(const KernelFamily& F, uint64_t n);
-void launch_perm_tablewise(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
+// false: no scratch could be allocated (the caller runs the document-outer kernel)
+bool launch_perm_tablewise(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
                            const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
                            uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
 
@@ -66,5 +67,22 @@ void count_launches(uint64_t n);
 // and the zero-copy path's reads and writes of mapped host memory).
 void count_transfer(uint64_t h2d, uint64_t d2h);
 void transfer_counts(uint64_t& h2d, uint64_t& d2h);
+
+// Path counters (bbmh_ext_counter): which of the library's routes ran.
+enum class Counter : int {
+    PeerCopyBytes,   // permutation tables replicated with cudaMemcpyPeer
+    ZeroCopyCalls,   // host calls served by the zero-copy small-batch path
+    Delta16Chunks,   // host chunks whose ids crossed as 16-bit differences
+    RawChunks,       // host chunks whose ids crossed as 4-byte ids (or were device-resident)
+    RangeShards,     // LibSVM text ranges sketched by range-sharded lanes
+    DeviceIdBatches, // loader batches whose ids never left the parsing GPU
+    kCount
+};
+void count(Counter c, uint64_t n = 1);
+inline void count_peer_copy(uint64_t bytes) { count(Counter::PeerCopyBytes, bytes); }
+// by name: "kernel_launches", "h2d_bytes", "d2h_bytes", "peer_copy_bytes",
+// "zero_copy_calls", "delta16_chunks", "raw_chunks", "range_shards",
+// "device_id_batches"; false if unknown
+bool counter_value(const char* name, uint64_t* out);
 
 }  // namespace bbmh

@@ -24,6 +24,7 @@
 #include <string>
 
 #include "core.hpp"
+#include "options.hpp"
 #include "engine.hpp"
 #include "kernels.cuh"
 
@@ -252,15 +253,11 @@ void grow_dev(T*& p, uint64_t& cap, uint64_t need) {
 
 }  // namespace
 
-bool gpu_parse_enabled() {
-    const char* e = std::getenv("BBMH_GPU_PARSE");
-    return !(e && *e == '0');
-}
+bool gpu_parse_enabled() { return opt(Opt::GpuParse) != 0; }
 
 uint64_t gpu_parse_block_bytes(uint64_t dflt) {
-    const char* e = std::getenv("BBMH_GPU_PARSE_BLOCK");  // developer/test knob
-    const uint64_t v = e && *e ? std::strtoull(e, nullptr, 10) : 0;
-    return v >= 64 ? v : dflt;
+    const int64_t v = opt(Opt::GpuParseBlock);
+    return v >= 64 ? uint64_t(v) : dflt;
 }
 
 GpuLibsvmParser::GpuLibsvmParser(int device) : device_(device) {

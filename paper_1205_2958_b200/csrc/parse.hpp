@@ -111,8 +111,8 @@ private:
     size_t scan_tmp_bytes_ = 0;
 };
 
-// BBMH_GPU_PARSE=0 disables the device parser (CPU parsing only); read when a
-// reader is opened. BBMH_GPU_PARSE_BLOCK=<bytes> overrides the block size.
+// Option "gpu_parse" = 0 disables the device parser (CPU parsing only); read when a
+// reader is opened. Option "gpu_parse_block" (bytes) overrides the block size.
 bool gpu_parse_enabled();
 uint64_t gpu_parse_block_bytes(uint64_t dflt);
 

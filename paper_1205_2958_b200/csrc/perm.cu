@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "options.hpp"
 
 namespace bbmh {
 
@@ -157,42 +158,63 @@ void launch_pass(const KernelFamily& F, uint32_t j0, uint32_t gc, const uint64_t
 }  // namespace
 
 bool perm_tablewise_applies(const KernelFamily& F, uint64_t n) {
-    const char* e = std::getenv("BBMH_PERM_TABLEWISE");
-    if (e && *e) return std::atoi(e) != 0;
+    const int64_t mode = opt(Opt::PermTablewise);
+    if (mode >= 0) return mode != 0;
     const uint64_t table_bytes = (uint64_t)F.k * F.dim * 4;
     return table_bytes > (96ull << 20) && n >= 256;
 }
 
-void launch_perm_tablewise(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
+bool launch_perm_tablewise(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
                            const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
                            uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // The per-(doc, table) minima scratch is n*k*4 bytes; documents go in
+    // slices that keep it within the budget (each slice streams the tables
+    // through L2 once more). If even a small slice cannot be allocated the
+    // caller runs the document-outer kernel, which needs no scratch.
+    const uint64_t budget_bytes = (uint64_t)(opt(Opt::PermScratchMb) > 0 ? opt(Opt::PermScratchMb) : 2048) << 20;
+    uint64_t slice = budget_bytes / ((uint64_t)F.k * 4);
+    if (slice < 1) slice = 1;
+    if (slice > n) slice = n;
     uint32_t* min32 = nullptr;
-    if (cudaMallocAsync(&min32, n * F.k * sizeof(uint32_t), st) != cudaSuccess) return;
-    // tables per pass: as many as fit in ~80 MB of L2 (power of two, <= 32)
-    const uint64_t budget = 80ull << 20;
-    uint32_t G = 1;
-    while (G < 32 && (uint64_t)(2 * G) * F.dim * 4 <= budget && 2 * G <= F.k) G *= 2;
-    const int grid = sms * 8;
-    uint64_t passes = 0;
-    for (uint32_t j0 = 0; j0 < F.k; j0 += G, ++passes) {
-        const uint32_t gc = F.k - j0 < G ? F.k - j0 : G;
-        switch (G) {
-            case 1: launch_pass<1>(F, j0, gc, row_ptr, base, idx, n, min32, err, grid, st); break;
-            case 2: launch_pass<2>(F, j0, gc, row_ptr, base, idx, n, min32, err, grid, st); break;
-            case 4: launch_pass<4>(F, j0, gc, row_ptr, base, idx, n, min32, err, grid, st); break;
-            case 8: launch_pass<8>(F, j0, gc, row_ptr, base, idx, n, min32, err, grid, st); break;
-            case 16: launch_pass<16>(F, j0, gc, row_ptr, base, idx, n, min32, err, grid, st); break;
-            default: launch_pass<32>(F, j0, gc, row_ptr, base, idx, n, min32, err, grid, st); break;
-        }
+    while (cudaMallocAsync(&min32, slice * F.k * sizeof(uint32_t), st) != cudaSuccess) {
+        cudaGetLastError();
+        min32 = nullptr;
+        if (slice <= 256) return false;
+        slice /= 2;
     }
-    const uint64_t pg = n < (uint64_t)sms * 16 ? n : (uint64_t)sms * 16;
-    pack_minima_kernel<<<(unsigned)pg, 256, 0, st>>>(min32, row_ptr, n, F.k, b, codes, minima,
-                                                     flags, err);
+    // tables per pass: as many as fit in ~80 MB of L2 (power of two, <= 32)
+    const uint64_t l2_budget = 80ull << 20;
+    uint32_t G = 1;
+    while (G < 32 && (uint64_t)(2 * G) * F.dim * 4 <= l2_budget && 2 * G <= F.k) G *= 2;
+    const int grid = sms * 8;
+    const uint64_t cb = ((uint64_t)F.k * b + 7) >> 3;
+    uint64_t launches = 0;
+    for (uint64_t d0 = 0; d0 < n; d0 += slice) {
+        const uint64_t m = n - d0 < slice ? n - d0 : slice;
+        const uint64_t* rp = row_ptr + d0;
+        for (uint32_t j0 = 0; j0 < F.k; j0 += G, ++launches) {
+            const uint32_t gc = F.k - j0 < G ? F.k - j0 : G;
+            switch (G) {
+                case 1: launch_pass<1>(F, j0, gc, rp, base, idx, m, min32, err, grid, st); break;
+                case 2: launch_pass<2>(F, j0, gc, rp, base, idx, m, min32, err, grid, st); break;
+                case 4: launch_pass<4>(F, j0, gc, rp, base, idx, m, min32, err, grid, st); break;
+                case 8: launch_pass<8>(F, j0, gc, rp, base, idx, m, min32, err, grid, st); break;
+                case 16: launch_pass<16>(F, j0, gc, rp, base, idx, m, min32, err, grid, st); break;
+                default: launch_pass<32>(F, j0, gc, rp, base, idx, m, min32, err, grid, st); break;
+            }
+        }
+        const uint64_t pg = m < (uint64_t)sms * 16 ? m : (uint64_t)sms * 16;
+        pack_minima_kernel<<<(unsigned)pg, 256, 0, st>>>(min32, rp, m, F.k, b, codes + d0 * cb,
+                                                         minima ? minima + d0 * F.k : nullptr,
+                                                         flags ? flags + d0 : nullptr, err);
+        ++launches;
+    }
     cudaFreeAsync(min32, st);
-    count_launches(passes + 1);
+    count_launches(launches);
+    return true;
 }
 
 }  // namespace bbmh

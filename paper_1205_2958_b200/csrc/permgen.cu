@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "core.hpp"
+#include "options.hpp"
 #include "engine.hpp"
 #include "kernels.cuh"
 
@@ -110,8 +111,7 @@ __global__ void __launch_bounds__(128) perm_shuffle_warp_kernel(uint32_t* __rest
 }  // namespace
 
 bool build_perm_tables_gpu(Family& f) {
-    const char* e = std::getenv("BBMH_GPU_PERMGEN");
-    if (e && *e == '0') return false;
+    if (!opt(Opt::GpuPermgen)) return false;
     const uint64_t dim = f.dim, k = f.k;
     const size_t bytes = size_t(dim) * k * sizeof(uint32_t);
     if (dim < 2 || bytes < (size_t(64) << 20)) return false;  // small: the host is as fast

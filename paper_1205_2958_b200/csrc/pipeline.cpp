@@ -21,6 +21,7 @@
 
 #include "engine.hpp"
 #include "io.hpp"
+#include "options.hpp"
 
 namespace bbmh {
 
@@ -204,10 +205,7 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
 
     // One GPU that also parses the text: its batches keep their ids on the
     // device (no D2H after parsing, no H2D before sketching).
-    const bool device_ids = devs.size() == 1 && reader.parser_device() == devs[0] && [] {
-        const char* e = std::getenv("BBMH_DEVICE_IDS");  // developer knob (A/B timing)
-        return !(e && *e == '0');
-    }();
+    const bool device_ids = devs.size() == 1 && reader.parser_device() == devs[0] && opt(Opt::DeviceIds);
     const size_t nbatches = 3 * devs.size() + 3;
     BatchLease storage(nbatches);  // pinned batches reused across calls
     trace("stream: batches leased");

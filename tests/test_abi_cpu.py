@@ -110,3 +110,41 @@ def test_out_of_scope_symbols_report_not_provided(bb):
     fn.restype = C.c_int32
     assert fn(None, None, None, None, None) == bb.E_INTERNAL
     assert "not provided" in bb.last_error()
+
+
+def test_options_table_and_counters(bb):
+    """Every switch is an option (no getenv on a call path): known names
+    round-trip, unknown ones fail with INVALID_ARGUMENT, counters exist."""
+    names = bb.option_names()
+    for nm in ("carveout", "delta16", "host_sharers", "zero_copy", "range_shards",
+               "perm_tablewise", "gpu_parse", "force_peer_copy", "trace"):
+        assert nm in names, nm
+    old = bb.get_option("chunk_ids")
+    with bb.option(chunk_ids=123456):
+        assert bb.get_option("chunk_ids") == 123456
+    assert bb.get_option("chunk_ids") == old
+    with pytest.raises(bb.BbmhError) as ex:
+        bb.set_option("no_such_option", 1)
+    assert ex.value.status == bb.E_INVALID_ARGUMENT
+    for c in ("kernel_launches", "h2d_bytes", "d2h_bytes", "peer_copy_bytes", "zero_copy_calls",
+              "delta16_chunks", "raw_chunks", "range_shards", "device_id_batches"):
+        assert bb.counter(c) >= 0
+    with pytest.raises(bb.BbmhError):
+        bb.counter("no_such_counter")
+
+
+def test_no_getenv_on_call_paths():
+    """Only options.cpp reads the environment (once, at first use)."""
+    csrc = os.path.join(ROOT, "paper_1205_2958_b200", "csrc")
+    readers = [f for f in os.listdir(csrc)
+               if f.endswith((".cu", ".cpp", ".hpp", ".cuh")) and "getenv" in open(os.path.join(csrc, f)).read()]
+    assert readers == ["options.cpp"], readers
+
+
+def test_codes_out_is_validated(bb):
+    with bb.Family(1, 1 << 20, 64, 1) as f:
+        rp = np.array([0, 2], np.uint64)
+        idx = np.array([1, 2], np.uint32)
+        for bad in (np.zeros(3, np.uint8), np.zeros(64, np.uint16), np.zeros((2, 64), np.uint8)[:, ::2]):
+            with pytest.raises(ValueError):
+                f.sketch_csr(rp, idx, 8, codes_out=bad)

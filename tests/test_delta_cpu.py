@@ -18,7 +18,7 @@ def test_delta16_encoder_round_trip(tmp_path):
     cuda_inc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "include")
     subprocess.run(["g++", "-O2", "-std=c++20", "-I", cuda_inc, "-I", CSRC, "-o", exe,
                     os.path.join(ROOT, "tests", "cpu", "delta_roundtrip.cpp"),
-                    os.path.join(CSRC, "delta.cpp"), os.path.join(CSRC, "hostpool.cpp"), "-lpthread"],
+                    os.path.join(CSRC, "delta.cpp"), os.path.join(CSRC, "hostpool.cpp"), os.path.join(CSRC, "options.cpp"), "-lpthread"],
                    check=True)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300, check=True).stdout
     assert "trials 300 bad 0" in out, out

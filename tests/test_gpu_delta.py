@@ -24,7 +24,7 @@ def _csr(rows):
 
 
 def _run(bb, f, rp, idx, b, mode, pinned=False, chunk_docs=0):
-    os.environ["BBMH_DELTA_H2D"] = mode
+    bb.set_option("delta16", -1 if mode == "auto" else int(mode))
     pin = None
     try:
         if chunk_docs:
@@ -38,7 +38,7 @@ def _run(bb, f, rp, idx, b, mode, pinned=False, chunk_docs=0):
         codes, _, flags = f.sketch_csr(rp, arr, b)
         return codes, flags, bb.kernel_launches() - l0
     finally:
-        os.environ.pop("BBMH_DELTA_H2D", None)
+        bb.set_option("delta16", -1)
         bb.set_chunk_docs(0)
         if pin is not None:
             pin.free()
@@ -110,7 +110,7 @@ def test_delta_transfer_auto_on_webspam_shape(bb):
     rng = np.random.default_rng(41)
     rp, idx = random_csr(rng, 4000, 1 << 24, 3000, 4400)  # 4 chunks of ~3.7 Mi ids
     f = bb.Family(1, 1 << 24, 500, 42)
-    os.environ.pop("BBMH_DELTA_H2D", None)
+    bb.set_option("delta16", -1)
     l0 = bb.kernel_launches()
     x0 = bb.transfer_bytes()[0]
     auto = f.sketch_csr(rp, idx, 8)[0]

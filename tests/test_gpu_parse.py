@@ -47,11 +47,8 @@ def _corpus(rng, n, mixed):
 
 
 def _sketch(bb, path, out, gpu, block=None):
-    os.environ["BBMH_GPU_PARSE"] = "1" if gpu else "0"
-    if block:
-        os.environ["BBMH_GPU_PARSE_BLOCK"] = str(block)
-    else:
-        os.environ.pop("BBMH_GPU_PARSE_BLOCK", None)
+    bb.set_option("gpu_parse", 1 if gpu else 0)
+    bb.set_option("gpu_parse_block", block or 0)
     try:
         l0 = bb.kernel_launches()
         with bb.Family(1, 1 << 22, 64, 42) as f:
@@ -62,8 +59,8 @@ def _sketch(bb, path, out, gpu, block=None):
                 res = (e.status, str(e))
         return res, bb.kernel_launches() - l0
     finally:
-        os.environ.pop("BBMH_GPU_PARSE", None)
-        os.environ.pop("BBMH_GPU_PARSE_BLOCK", None)
+        bb.set_option("gpu_parse", 1)
+        bb.set_option("gpu_parse_block", 0)
 
 
 @pytest.mark.parametrize("mixed", [False, True])
@@ -85,11 +82,8 @@ def test_gpu_parse_matches_cpu_and_reference(bb, ref, tmp_path, mixed):
         if not mixed:
             assert launches > 4, "the GPU parser did not run"
     # ids copied back to the host after parsing, instead of kept on the device
-    os.environ["BBMH_DEVICE_IDS"] = "0"
-    try:
+    with bb.option(device_ids=0):
         (g, _) = _sketch(bb, str(path), str(tmp_path / "gpu2.bbmh"), gpu=True, block=1 << 16)
-    finally:
-        os.environ.pop("BBMH_DEVICE_IDS")
     assert g == cpu, mixed
 
 

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 def test_perm_schedules_match_oracle(bb, port, tablewise, dim, k):
     rng = np.random.default_rng(dim + k)
     rp, idx = random_csr(rng, 300, dim, 0, 400, empty_every=11)
-    os.environ["BBMH_PERM_TABLEWISE"] = tablewise
+    bb.set_option("perm_tablewise", int(tablewise))
     try:
         f = bb.Family(0, dim, k, 77, 0, 1 << 31)
         for b in (1, 8, 13, 32):
@@ -29,16 +29,16 @@ def test_perm_schedules_match_oracle(bb, port, tablewise, dim, k):
             assert np.array_equal(minima, m2)
             assert np.array_equal(flags, f2)
     finally:
-        os.environ.pop("BBMH_PERM_TABLEWISE", None)
+        bb.set_option("perm_tablewise", -1)
 
 
 def test_perm_tablewise_out_of_range_is_an_error(bb):
     rp = np.array([0, 2] + [2] * 300, np.uint64)
-    os.environ["BBMH_PERM_TABLEWISE"] = "1"
+    bb.set_option("perm_tablewise", 1)
     try:
         f = bb.Family(0, 1000, 4, 1)
         with pytest.raises(bb.BbmhError) as ex:
             f.sketch_csr(rp, np.array([5, 1000], np.uint32), 8)
         assert ex.value.status == bb.E_INVALID_ARGUMENT
     finally:
-        os.environ.pop("BBMH_PERM_TABLEWISE", None)
+        bb.set_option("perm_tablewise", -1)

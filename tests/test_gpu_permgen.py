@@ -1,7 +1,7 @@
 """Permutation tables built on the GPU (csrc/permgen.cu) are the reference's
 tables: every entry of random tables equals the host build (bbmh_family_map
 through the C ABI reads the device tables back), and sketches agree with the
-oracle; the host build (BBMH_GPU_PERMGEN=0) gives identical sketches."""
+oracle; the host build (option gpu_permgen = 0) gives identical sketches."""
 import os
 
 import numpy as np
@@ -25,14 +25,14 @@ def test_gpu_built_tables_match_reference(bb, port, dim, k):
     codes, minima, flags = f.sketch_csr(rp, idx, 8, want_minima=True)
     s, c2, m2, f2 = port.sketch_csr(h, k, rp, idx, 8)
     assert s == 0 and np.array_equal(codes, c2) and np.array_equal(minima, m2)
-    os.environ["BBMH_GPU_PERMGEN"] = "0"
+    bb.set_option("gpu_permgen", 0)
     try:
         g = bb.Family(0, dim, k, 42, 0, 1 << 34)
         c3, m3, _ = g.sketch_csr(rp, idx, 8, want_minima=True)
         assert np.array_equal(codes, c3) and np.array_equal(minima, m3)
         g.close()
     finally:
-        os.environ.pop("BBMH_GPU_PERMGEN")
+        bb.set_option("gpu_permgen", 1)
     port.destroy(h)
     f.close()
 

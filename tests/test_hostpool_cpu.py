@@ -16,6 +16,6 @@ def test_host_pool(tmp_path):
     exe = str(tmp_path / "hostpool_test")
     subprocess.run(["g++", "-O2", "-std=c++20", "-I", CSRC, "-o", exe,
                     os.path.join(ROOT, "tests", "cpu", "hostpool_test.cpp"),
-                    os.path.join(CSRC, "hostpool.cpp"), "-lpthread"], check=True)
+                    os.path.join(CSRC, "hostpool.cpp"), os.path.join(CSRC, "options.cpp"), "-lpthread"], check=True)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "hostpool ok" in out.stdout, out.stdout + out.stderr

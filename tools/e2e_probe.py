@@ -1,5 +1,5 @@
 """e2e (host buffers through bbmh_ext_sketch_csr) at the webspam shape with the
-id transfer as 4-byte ids (BBMH_DELTA_H2D=0), as 2-byte differences (=1) and
+id transfer as 4-byte ids (option delta16 = 0), as 2-byte differences (=1) and
 by default; pinned and pageable inputs. One JSON line per case."""
 import json
 import os
@@ -28,10 +28,7 @@ ref = None
 for mode in os.environ.get("E2E_MODES", "0,1,auto").split(","):
     mode = None if mode == "auto" else mode
     for pinned in (True, False):
-        if mode is None:
-            os.environ.pop("BBMH_DELTA_H2D", None)
-        else:
-            os.environ["BBMH_DELTA_H2D"] = mode
+        bbmh.set_option("delta16", -1 if mode is None else int(mode))
         arr = pin.array if pinned else idx
         fam.sketch_csr(rp, arr, 8, codes_out=out.array)
         ts = []

@@ -34,16 +34,16 @@ def main():
             f.sketch_set(idx[: int(rp[1])], 3)
             f.sketch_score_csr(rp, idx, 4, rng.standard_normal(k << 4))
     # ids through the 2-byte transfer (delta.cu): escapes, empty rows, a long row
-    os.environ["BBMH_DELTA_H2D"] = "1"
+    bbmh.set_option("delta16", 1)
     with bbmh.Family(1, 1 << 20, 70, 42) as f:
         f.sketch_csr(rp, idx, 8)
         f.sketch_csr(long_rp, long_idx, 8)
         f.sketch_csr(rp, np.ascontiguousarray(idx[::-1]), 8)
-    os.environ.pop("BBMH_DELTA_H2D")
-    os.environ["BBMH_PERM_TABLEWISE"] = "1"
+    bbmh.set_option("delta16", -1)
+    bbmh.set_option("perm_tablewise", 1)
     with bbmh.Family(0, 1 << 12, 9, 42) as f:
         f.sketch_csr(rp, idx % (1 << 12), 6, want_minima=True)
-    os.environ["BBMH_PERM_TABLEWISE"] = "0"
+    bbmh.set_option("perm_tablewise", 0)
     with bbmh.Family(0, 1 << 12, 9, 42) as f:
         f.sketch_csr(rp, idx % (1 << 12), 6)
     # >= 64 MB of tables: built on the GPU (permgen.cu), read back by map()
@@ -61,9 +61,9 @@ def main():
             txt = os.path.join(td, "c.txt")
             lines = ["%+d" % lab + "".join(" %d:1" % (t + 1) for t in ids) for lab, ids in rows]
             open(txt, "w").write("\n".join(lines) + "\n\n0\n+1 5:1 # c\n")
-            os.environ["BBMH_GPU_PARSE_BLOCK"] = "4096"
+            bbmh.set_option("gpu_parse_block", 4096)
             f.sketch_file(txt, os.path.join(td, "t.bbmh"), 4, 5, 2)
-            os.environ.pop("BBMH_GPU_PARSE_BLOCK")
+            bbmh.set_option("gpu_parse_block", 0)
             f.sketch_file(txt, os.path.join(td, "t2.bbmh"), 4, 5, 2)
         bbmh.expand_file(sk, os.path.join(td, "e.txt"), bbmh.ROWS_LIBSVM)
         bbmh.expand_file(sk, os.path.join(td, "e.bbcv"), bbmh.ROWS_BINARY)

@@ -1,4 +1,4 @@
-"""Trace the BBCV file pipeline (BBMH_TRACE=1) on a webspam-shaped binary corpus."""
+"""Trace the BBCV file pipeline (BBMH_OPT_TRACE=1) on a webspam-shaped binary corpus."""
 import os, sys, time, tempfile
 import numpy as np
 sys.path.insert(0, os.getcwd())

@@ -1,4 +1,4 @@
-"""Trace the LibSVM file pipeline (BBMH_TRACE) on a webspam-shaped text corpus."""
+"""Trace the LibSVM file pipeline (BBMH_OPT_TRACE) on a webspam-shaped text corpus."""
 import os
 import sys
 import tempfile
@@ -6,7 +6,7 @@ import time
 
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("BBMH_TRACE", "0")
+os.environ.setdefault("BBMH_OPT_TRACE", "0")
 import bench  # noqa: E402
 from paper_1205_2958_b200 import bbmh  # noqa: E402
 
@@ -23,7 +23,7 @@ f = bbmh.Family(1, 1 << 24, 500, 42)
 f.prepare(0)
 for i in range(4):
     for mode in ("1", "0"):
-        os.environ["BBMH_GPU_PARSE"] = mode
+        bbmh.set_option("gpu_parse", int(mode))
         t = time.perf_counter()
         st = f.sketch_file(path, os.path.join(td, "o.bbmh"), 8, 10000, os.cpu_count())
         dt = time.perf_counter() - t

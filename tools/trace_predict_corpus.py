@@ -1,6 +1,6 @@
 import sys, os, time, json, ctypes as C, numpy as np, tempfile
 sys.path.insert(0, '/root/repo')
-os.environ['BBMH_TRACE'] = '1'
+os.environ['BBMH_OPT_TRACE'] = '1'
 from oracle import oracle as O
 from paper_1205_2958_b200 import bbmh
 R = O.ref(); L = R.lib

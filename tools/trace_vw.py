@@ -1,6 +1,6 @@
 import os, sys, time, tempfile, ctypes as C
 sys.path.insert(0, '/root/repo')
-os.environ['BBMH_TRACE'] = '1'
+os.environ['BBMH_OPT_TRACE'] = '1'
 from oracle import oracle as O
 from paper_1205_2958_b200 import bbmh
 R = O.ref(); L = R.lib

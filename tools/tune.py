@@ -1,6 +1,6 @@
 """Sweep launch knobs (J, threads per CTA, CTAs per SM, smem tile) for the
 sketch kernel on an HBM-resident webspam-shaped corpus; prints ms and
-T evals/s per setting. Developer tool (env knobs BBMH_TUNE_*)."""
+T evals/s per setting. Developer tool (bbmh_ext_set_option switches)."""
 import itertools
 import json
 import os
@@ -30,23 +30,20 @@ def main():
     for scheme in schemes:
         sid, dim = bench.SCHEMES[scheme]
         fam = bbmh.Family(sid, dim, K, bench.SEED)
-        for k_ in ("J", "TPB", "TILE", "CTAS_PER_SM", "G"):
-            os.environ.pop("BBMH_TUNE_" + k_, None)
+        for k_ in ("shape_j", "shape_tpb", "tile", "ctas_per_sm"):
+            bbmh.set_option(k_, 0)
         fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, bench.B,
                               d_codes.data_ptr(), stream=st.cuda_stream)
         torch.cuda.synchronize()
         ref_codes = d_codes.clone()
         for g in grid:
-            if g.get("J", 0):
-                os.environ["BBMH_TUNE_J"] = str(g["J"])
-                os.environ["BBMH_TUNE_TPB"] = str(g["TPB"])
-            else:  # the library's own shape for this k
-                os.environ.pop("BBMH_TUNE_J", None)
-                os.environ.pop("BBMH_TUNE_TPB", None)
-            os.environ["BBMH_TUNE_TILE"] = str(g["TILE"])
-            os.environ["BBMH_TUNE_CTAS_PER_SM"] = str(g.get("CTAS", 0))
-            os.environ["BBMH_TUNE_SMEM_CAP"] = str(g.get("SMEM_CAP", 1))
-            os.environ["BBMH_TUNE_G"] = str(g.get("G", 4))
+            # (J = 0: the library's own shape for this k)
+            bbmh.set_option("shape_j", g.get("J", 0))
+            bbmh.set_option("shape_tpb", g.get("TPB", 0) if g.get("J", 0) else 0)
+            bbmh.set_option("tile", g.get("TILE", 0))
+            bbmh.set_option("ctas_per_sm", g.get("CTAS", 0))
+            bbmh.set_option("smem_cap", g.get("SMEM_CAP", 1))
+            bbmh.set_option("carveout", g.get("CARVEOUT", -1))
 
             def step():
                 fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, bench.B,

@@ -51,7 +51,7 @@ def main():
                   np.array_equal(p_flags.array, ref_flags))
         t_zc = p50(zc)
         t_host = p50(lambda: fam.sketch_csr(rp, p_idx.array, b))
-        print(json.dumps({"scheme": scheme, "batch": batch, "mode": os.environ.get("BBMH_ZERO_COPY", "1"),
+        print(json.dumps({"scheme": scheme, "batch": batch, "mode": bbmh.get_option("zero_copy"),
                           "device_api_on_pinned_us": round(t_zc, 1),
                           "host_api_us": round(t_host, 1), "identical": ok}), flush=True)
         for a in (p_rp, p_idx, p_codes, p_flags):
