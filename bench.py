@@ -17,11 +17,20 @@ step streams it from HBM.
            D2H of codes+flags all inside the timed region (wall clock);
   cpu_baseline = the unmodified reference (oracle/_ref, bbmh_sketch_set on
            all host threads) on a bounded prefix sample, rank 0, N = 1.
+  schemes.perm = config 3 (permutation tables, D = 2^24, k = 500: 31.25 GiB
+           built on the GPU) over the same 350,000 documents.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c4]
 Multi-GPU: launched by torch.distributed.run, one rank per GPU, documents
 sharded (each rank sketches its own 350k-doc corpus: weak scaling), no
 collective on the data path; the timing max is taken with one all-reduce.
+
+--config c4 (BASELINE.json configs[3], the rcv1-expanded shape): value is the
+4U-bit kernel over the full 677,399 x 12,000-id corpus resident in HBM
+(32.5 GB); e2e is bbmh_sketch_file on a synthetic LibSVM text of that shape
+generated on the box (~21 GB by default), with the read / parse / hash /
+write split and the hash-vs-load ratio.
 """
 from __future__ import annotations
 
@@ -45,7 +54,20 @@ D_2U = 1 << 24
 K = 500
 B = 8
 SEED = 42
-SCHEMES = {"2u": (1, D_2U), "4u-bit": (3, D_WEBSPAM), "4u-mod": (2, D_WEBSPAM)}
+SCHEMES = {"2u": (1, D_2U), "4u-bit": (3, D_WEBSPAM), "4u-mod": (2, D_WEBSPAM), "perm": (0, D_2U)}
+# config 4 (rcv1-expanded shape)
+C4_DOCS = 677_399
+C4_NNZ = 12_000
+C4_DIM = 1_010_017_424
+C4_DIM_2U = 1 << 30
+
+# SURVEY.md §8d fixed algorithmic contract: hash evaluations per SM clock at
+# the integer-pipe peak (2U: IMAD + IMNMX on separate pipes, 64/clk; 4U-bit:
+# 12 ALU-only ops per evaluation on the 64/clk ALU pipe). Fixed, not
+# re-measured per run: 18.6 T and 1.55 T evaluations/s at 1,965 MHz.
+CONTRACT_EVALS_PER_SM_CLK = {"2u": 64.0, "4u-bit": 64.0 / 12, "4u-mod": 64.0 / 12}
+SMS = 148
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, only without MEASURED_PEAKS.json
 
 
 def log(*a):
@@ -98,6 +120,28 @@ def make_corpus_host(n, nnz, dim, seed):
     u = np.sort(rng.random((n, nnz)), axis=1)
     ids = (u * (dim - nnz)).astype(np.int64) + np.arange(nnz)
     return (np.arange(n + 1, dtype=np.uint64) * nnz), ids.reshape(-1).astype(np.uint32)
+
+
+def hbm_peak():
+    """HBM copy bandwidth (GB/s) from the driver-written MEASURED_PEAKS.json."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
+
+
+def host_info():
+    """Host CPU model and thread count (recorded beside every CPU number)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def workload_config(docs_per_gpu, world, **extra):
@@ -205,6 +249,23 @@ def pipe_costs(scheme, dim, peaks):
     return None, None
 
 
+def roofline_contract(scheme, evals_per_s, sm_mhz, pipe_model=None):
+    """Integer roofline against the fixed SURVEY §8d contract, at the SM clock
+    sampled under load (and at the 1,965 MHz maximum)."""
+    epc = CONTRACT_EVALS_PER_SM_CLK.get(scheme)
+    if epc is None or not sm_mhz:
+        return None
+    peak = SMS * epc * sm_mhz * 1e6
+    peak_max = SMS * epc * 1965e6
+    out = {"bound": "int", "unit": "Gevals/s", "achieved": evals_per_s / 1e9, "peak": peak / 1e9,
+           "frac": evals_per_s / peak, "frac_at_1965mhz": evals_per_s / peak_max,
+           "evals_per_sm_clk_peak": epc, "sm_mhz": sm_mhz,
+           "peak_how": "SURVEY.md §8d fixed contract: 148 SMs x evals/clk/SM x SM clock under load"}
+    if pipe_model:
+        out["pipe_model"] = pipe_model
+    return out
+
+
 def roofline_int(scheme, dim, evals_per_s, sm_mhz, peaks):
     """Integer-pipe roofline of the sketch kernel: the slower of the fma-heavy
     and alu pipes at their measured per-SM rates and the SM clock under load."""
@@ -243,6 +304,8 @@ def run_reference(args):
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
+    if args.config == "c4":
+        return run_c4_reference(args)
     scheme_id, dim = SCHEMES[args.scheme]
     threads = os.cpu_count() or 1
     nc = 4 * threads
@@ -264,18 +327,38 @@ def run_reference(args):
         secs.append(s)
     t = float(np.mean(secs))
     v = evals / t
+    sample = (f"{n_sample} webspam-shaped docs per step (of {N_DOCS}); the rate is extrapolated "
+              f"to the {N_DOCS}-doc workload (cost per evaluation is size-independent); "
+              "bbmh_sketch_set on all host threads")
     print(json.dumps({
         "impl": "reference", "metric": "hash_evals_per_sec", "value": v, "unit": "hash-evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": workload_config(N_DOCS, 1, reference_sample_docs=n_sample),
+        "config": workload_config(N_DOCS, 1, reference_sample_docs=n_sample, extrapolated=True),
         "docs_per_sec": n_sample / t,
         "cpu_baseline": {"value": v, "unit": "hash-evals/s", "cores": threads, "kind": "reference",
-                         "sample": f"{n_sample} webspam-shaped docs per step (of {N_DOCS}), "
-                                   "bbmh_sketch_set on all host threads"},
+                         "extrapolated": True, "sample": sample, **host_info()},
         "e2e": {"value": v, "unit": "hash-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def time_steps(torch, stream, step, steps, warmup, barrier, max_over_ranks):
+    """W untimed steps, then K steps between CUDA events on `stream` (barrier and
+    synchronize on both sides); ms per step as the max over ranks, and per-step
+    times."""
+    for _ in range(warmup):
+        step()
+    barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    barrier()
+    ev[0].record(stream)
+    for i in range(steps):
+        step()
+        ev[i + 1].record(stream)
+    barrier()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return max_over_ranks(ev[0].elapsed_time(ev[-1]) / steps), per
 
 
 def run_ours(args):
@@ -299,20 +382,30 @@ def run_ours(args):
     from paper_1205_2958_b200 import _build
     if not os.path.exists(os.path.join(ROOT, "paper_1205_2958_b200", "libbbmh.so")):
         _build.build()
-    from paper_1205_2958_b200 import bbmh
+    from paper_1205_2958_b200 import bbmh, shard
+    # the ranks of this job on this node share its DRAM and cores: the library's
+    # id-transfer budget counts them (the launcher knows, the library does not)
+    shard.configure_host_sharing()
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
+    def gather_over_ranks(x):
         if world == 1:
-            return x
+            return [x]
         on = dev if dist.get_backend() == "nccl" else torch.device("cpu")
         t = torch.tensor([x], dtype=torch.float64, device=on)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        out = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return [float(o.item()) for o in out]
+
+    def max_over_ranks(x):
+        return max(gather_over_ranks(x))
+
+    if args.config == "c4":
+        return run_c4(args, torch, dev, rank, world, local, barrier, max_over_ranks, bbmh)
 
     n, nnz = args.docs, NNZ
     t0 = time.time()
@@ -325,47 +418,51 @@ def run_ours(args):
     d_flags = torch.empty(n, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     peaks = int_peaks() if rank == 0 else None
+    hbm_gbs, hbm_src = hbm_peak()
 
     launches0 = bbmh.kernel_launches()
     results = {}
     clocks = None
     for name in args.schemes.split(","):
         scheme_id, dim = SCHEMES[name]
-        fam = bbmh.Family(scheme_id, dim, K, SEED)
+        steps, warmup = args.steps, args.warmup
+        t_build = time.perf_counter()
+        fam = bbmh.Family(scheme_id, dim, K, SEED, 0, dim * K * 4 + (1 << 20) if name == "perm" else 0)
         fam.prepare(local)
+        build_s = time.perf_counter() - t_build
+        if name == "perm":
+            # ~2.5 s per step: a bounded number of steps keeps the default run short
+            steps, warmup = min(steps, args.perm_steps), min(warmup, 3)
 
         def step():
             fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, B, d_codes.data_ptr(),
                                   None, d_flags.data_ptr(), stream=stream.cuda_stream)
 
-        for _ in range(args.warmup):
-            step()
-        barrier()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         with ClockSampler(local) as cs:
-            barrier()
-            ev[0].record(stream)
-            for i in range(args.steps):
-                step()
-                ev[i + 1].record(stream)
-            barrier()
-        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-        ms = max_over_ranks(ev[0].elapsed_time(ev[-1]) / args.steps)
+            ms, per = time_steps(torch, stream, step, steps, warmup, barrier, max_over_ranks)
         clk = cs.summary()
         if name == "2u":
             clocks = clk
         ev_s = evals * world / (ms * 1e-3)
         results[name] = {"hash_evals_per_sec": ev_s, "docs_per_sec": n * world / (ms * 1e-3),
                          "ms_per_step": ms, "kernel_ms_min": min(per), "kernel_ms_max": max(per),
-                         "sm_mhz": clk["sm_mhz"]}
+                         "steps": steps, "warmup": warmup, "sm_mhz": clk["sm_mhz"]}
         if rank == 0:
-            rl = roofline_int(name, dim, evals / (ms * 1e-3), clk["sm_mhz"], peaks)
-            results[name]["roofline"] = rl
+            if name == "perm":
+                results[name]["table_bytes"] = dim * K * 4
+                results[name]["family_build_s"] = build_s
+                results[name]["roofline"] = roofline_perm(evals / (ms * 1e-3), hbm_gbs)
+            else:
+                pm = roofline_int(name, dim, evals / (ms * 1e-3), clk["sm_mhz"], peaks)
+                results[name]["roofline"] = roofline_contract(name, evals / (ms * 1e-3), clk["sm_mhz"], pm)
             alg_bytes = n * nnz * 4 + (n + 1) * 8 + n * cb + n
             results[name]["hbm_gbs_algorithmic"] = alg_bytes / (ms * 1e-3) / 1e9
+            rl = results[name]["roofline"]
             log(f"[{name}] {ms:.2f} ms/step  {ev_s / 1e12:.3f} T evals/s  "
                 f"frac={rl['frac'] if rl else None}  clocks={clk}")
         fam.close()
+        del fam
+        torch.cuda.empty_cache()
     launches_kernel = bbmh.kernel_launches() - launches0
 
     # ---- e2e through the C ABI from pinned host buffers (2U) ----------------
@@ -374,18 +471,23 @@ def run_ours(args):
     pin = bbmh.PinnedArray(n * nnz, np.uint32)
     pin.array[:] = d_idx.cpu().numpy().view(np.uint32)
     codes_out = bbmh.PinnedArray(n * cb, np.uint8)
+    e2e_steps = args.e2e_steps or args.steps
     for _ in range(args.warmup):
         fam.sketch_csr(h_rp, pin.array, B, codes_out=codes_out.array)
     barrier()
     l0 = bbmh.kernel_launches()
     x0 = bbmh.transfer_bytes()
+    c0 = {c: bbmh.counter(c) for c in ("delta16_chunks", "raw_chunks", "zero_copy_calls")}
     t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
+    for _ in range(e2e_steps):
         codes, _, flags = fam.sketch_csr(h_rp, pin.array, B, codes_out=codes_out.array)
     barrier()
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+    my_e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_per_rank = gather_over_ranks(my_e2e_s)
+    e2e_s = max(e2e_per_rank)
     e2e_launches = bbmh.kernel_launches() - l0
     x1 = bbmh.transfer_bytes()
+    routes = {c: bbmh.counter(c) - v for c, v in c0.items()}
     # parity spot check of the e2e output against the device-resident run
     fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, B, d_codes.data_ptr(), None,
                           d_flags.data_ptr(), stream=stream.cuda_stream)
@@ -393,11 +495,12 @@ def run_ours(args):
     e2e_consistent = bool(np.array_equal(d_codes[: 1000 * cb].cpu().numpy(),
                                          codes_out.array[: 1000 * cb]))
     # bytes the library actually moved per step (ids go 2 B each as 16-bit row
-    # differences when the 4 B copy would bound the call: csrc/delta.hpp)
-    h2d = (x1[0] - x0[0]) // args.e2e_steps
-    d2h = (x1[1] - x0[1]) // args.e2e_steps
+    # differences when the host budget says that moves more ids/s: csrc/delta.hpp)
+    h2d = (x1[0] - x0[0]) // e2e_steps
+    d2h = (x1[1] - x0[1]) // e2e_steps
     ids_bytes = n * nnz * 4
     delta16 = h2d < ids_bytes
+    budget = bbmh.host_budget(max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))
     # host memory bandwidth: a pinned -> pinned copy on every host core (read + write)
     host_best = host_copy_gbps(bbmh)
     # the PCIe H2D copy bounds the 4-byte transfer: measure pinned H2D bandwidth here
@@ -430,9 +533,10 @@ def run_ours(args):
             secs, ref_codes = O.refbench_sketch_csr(O.REF_SO, 1, D_2U, K, SEED, srp, sidx, B, threads)
             parity = bool(np.array_equal(ref_codes.reshape(-1), codes_out.array[: ns * cb]))
             cpu = {"value": ns * nnz * K / secs, "unit": "hash-evals/s", "cores": threads,
-                   "kind": "reference", "parity_vs_gpu": parity,
+                   "kind": "reference", "parity_vs_gpu": parity, "extrapolated": True,
                    "sample": f"first {ns} of {n} docs, 2U k={K} b={B}, bbmh_sketch_set on "
-                             f"{threads} threads ({secs:.1f}s)"}
+                             f"{threads} threads ({secs:.1f}s); the rate is extrapolated to the "
+                             f"{n}-doc workload", **host_info()}
             log(f"[cpu] {cpu}")
     pin.free()
     codes_out.free()
@@ -450,6 +554,7 @@ def run_ours(args):
         if head.get("roofline") is not None:
             head["roofline"]["traffic"] = traffic.get("dram_bytes_per_launch")
             head["roofline"]["traffic_source"] = traffic.get("source")
+        e2e_rate = evals * world / e2e_s
         line = {
             "metric": "hash_evals_per_sec", "value": head["hash_evals_per_sec"],
             "unit": "hash-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -459,31 +564,35 @@ def run_ours(args):
             "docs_per_sec": head["docs_per_sec"],
             "roofline": head.get("roofline"),
             "roofline_hbm": {"bound": "hbm", "unit": "GB/s", "achieved": head.get("hbm_gbs_algorithmic"),
-                             "peak": 6461.2, "frac": (head.get("hbm_gbs_algorithmic") or 0) / 6461.2,
+                             "peak": hbm_gbs, "frac": (head.get("hbm_gbs_algorithmic") or 0) / hbm_gbs,
+                             "peak_source": hbm_src,
                              "traffic": traffic.get("dram_bytes_per_launch"),
                              "algorithmic_bytes_per_launch": n * nnz * 4 + (n + 1) * 8 + n * cb + n},
             "schemes": results,
-            "e2e": {"value": evals * world / e2e_s, "unit": "hash-evals/s",
+            "e2e": {"value": e2e_rate, "unit": "hash-evals/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s * 1e3, "api": "bbmh_ext_sketch_csr (pinned host CSR)",
-                    "consistent_with_device_run": e2e_consistent, "steps": args.e2e_steps,
+                    "consistent_with_device_run": e2e_consistent, "steps": e2e_steps,
+                    "per_rank_ms": [x * 1e3 for x in e2e_per_rank],
+                    "per_gpu_value": evals / e2e_s,
+                    "routes": routes, "host_budget": budget,
                     "transfer": ("ids as 16-bit row differences + escapes (csrc/delta.hpp), "
                                  "rebuilt on the GPU" if delta16 else "ids as u32"),
-                    "input_GBps": ids_bytes / e2e_s / 1e9,
-                    "roofline": ({"bound": "host_memory", "unit": "GB/s",
-                                  "achieved": 8 * n * nnz / e2e_s / 1e9, "peak": host_best,
-                                  "frac": 8 * n * nnz / e2e_s / 1e9 / host_best,
-                                  "traffic_model": "8 B per id of host DRAM traffic: the encode "
-                                                   "reads 4 and writes 2, the DMA reads 2",
-                                  "peak_how": "1 GiB pinned -> pinned copy on all host cores "
-                                              "(read + write), best of 3, this run"}
+                    "input_GBps": ids_bytes * world / e2e_s / 1e9,
+                    "roofline": ({"bound": "host_encode", "unit": "G ids/s",
+                                  "achieved": n * nnz * world / e2e_s / 1e9,
+                                  "peak": budget["encoded_ids_per_s"] / 1e9,
+                                  "frac": n * nnz * world / e2e_s / budget["encoded_ids_per_s"],
+                                  "peak_how": "bbmh_ext_host_budget: min(GPUs x link / 2 B, host encode "
+                                              "rate on all cores, measured by the library)"}
                                  if delta16 else
                                  {"bound": "pcie_h2d", "unit": "GB/s",
                                   "achieved": h2d / e2e_s / 1e9, "peak": pcie_gbs,
                                   "frac": h2d / e2e_s / 1e9 / pcie_gbs,
                                   "peak_how": "pinned 1 GiB torch copy_ H2D, best of 3, this run"}),
                     "pcie_h2d": {"achieved": h2d / e2e_s / 1e9, "peak": pcie_gbs,
-                                 "frac": h2d / e2e_s / 1e9 / pcie_gbs}},
+                                 "frac": h2d / e2e_s / 1e9 / pcie_gbs},
+                    "host_copy_gbps": host_best},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches_kernel + e2e_launches,
@@ -493,19 +602,258 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def roofline_perm(gathers_per_s, hbm_gbs):
+    """Permutation mode: one random 4-byte gather per evaluation. Against the
+    measured random-gather rate from a 64 MB L2-resident table on all SMs
+    (tools/intpeak.py l2_gathers, measured in this run) and the HBM sector
+    bound (one 32-byte sector per gather, the document-outer schedule)."""
+    out = {"bound": "l2_random_gather", "unit": "G gathers/s", "achieved": gathers_per_s / 1e9,
+           "hbm_sector_bound": hbm_gbs / 32, "hbm_sector_frac": gathers_per_s / 1e9 / (hbm_gbs / 32)}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import intpeak
+        l2 = intpeak.l2_gathers(sizes_mb=(64,))["64MB"]
+        out.update({"peak": l2, "frac": gathers_per_s / 1e9 / l2,
+                    "peak_how": "intpeak.l2_gathers: random 4 B loads from a 64 MB table, 8 x 256 "
+                                "threads per SM, this run"})
+    except Exception as e:  # noqa: BLE001
+        out["peak_error"] = str(e)
+    return out
+
+
+# ---- config 4: rcv1-expanded shape, streamed from LibSVM text ------------------
+
+def c4_corpus(args):
+    """Synthetic LibSVM text of the C4 row shape, generated on this host
+    (tools/gen_libsvm.cpp, all cores). Returns (path, bytes, docs)."""
+    d = args.c4_dir
+    os.makedirs(d, exist_ok=True)
+    exe = os.path.join(d, "gen_libsvm")
+    subprocess.run(["g++", "-O3", "-march=native", "-pthread", "-o", exe,
+                    os.path.join(ROOT, "tools", "gen_libsvm.cpp")], check=True)
+    path = os.path.join(d, f"rcv1_shape_{args.c4_text_docs}.txt")
+    t = time.perf_counter()
+    out = subprocess.run([exe, path, str(args.c4_text_docs), str(C4_NNZ), str(C4_DIM), "4242",
+                          str(os.cpu_count() or 1)], check=True, capture_output=True, text=True).stdout
+    info = json.loads(out)
+    log(f"[c4] text {info['bytes'] / 1e9:.1f} GB ({args.c4_text_docs} docs) generated in "
+        f"{time.perf_counter() - t:.1f}s")
+    return path, info["bytes"], args.c4_text_docs
+
+
+def c4_prefix(path, docs, out):
+    """The first `docs` lines of the text, for the reference's bounded sample."""
+    with open(path, "rb") as fi, open(out, "wb") as fo:
+        for _ in range(docs):
+            line = fi.readline()
+            if not line:
+                break
+            fo.write(line)
+    return out
+
+
+def run_c4(args, torch, dev, rank, world, local, barrier, max_over_ranks, bbmh):
+    hbm_gbs, hbm_src = hbm_peak()
+    cb = (K * B + 7) // 8
+    stream = torch.cuda.current_stream(dev)
+    # ---- value: 4U-bit over the full 677,399-doc corpus resident in HBM ----
+    n = args.c4_docs
+    t0 = time.time()
+    d_rp, d_idx = make_corpus_device(torch, n, C4_NNZ, C4_DIM, SEED + 1000 * rank, dev)
+    torch.cuda.synchronize()
+    log(f"[c4] device corpus {n} x {C4_NNZ} ({n * C4_NNZ * 4 / 1e9:.1f} GB) in {time.time() - t0:.1f}s")
+    d_codes = torch.empty(n * cb, dtype=torch.uint8, device=dev)
+    d_flags = torch.empty(n, dtype=torch.uint8, device=dev)
+    evals = n * C4_NNZ * K
+    kern = {}
+    launches0 = bbmh.kernel_launches()
+    clocks = None
+    for name, sid, dim in (("4u-bit", 3, C4_DIM), ("2u", 1, C4_DIM_2U)):
+        fam = bbmh.Family(sid, dim, K, SEED)
+        fam.prepare(local)
+
+        def step():
+            fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, B, d_codes.data_ptr(),
+                                  None, d_flags.data_ptr(), stream=stream.cuda_stream)
+
+        with ClockSampler(local) as cs:
+            ms, per = time_steps(torch, stream, step, args.steps, args.warmup, barrier, max_over_ranks)
+        clk = cs.summary()
+        if clocks is None:
+            clocks = clk
+        kern[name] = {"hash_evals_per_sec": evals * world / (ms * 1e-3), "ms_per_step": ms,
+                      "docs_per_sec": n * world / (ms * 1e-3), "dim": dim, "sm_mhz": clk["sm_mhz"],
+                      "roofline": roofline_contract(name, evals / (ms * 1e-3), clk["sm_mhz"])}
+        log(f"[c4 {name}] {ms:.1f} ms/step {evals / ms / 1e9:.3f} T evals/s")
+        fam.close()
+    del d_rp, d_idx, d_codes, d_flags
+    torch.cuda.empty_cache()
+    launches_kernel = bbmh.kernel_launches() - launches0
+
+    # ---- e2e: bbmh_sketch_file on LibSVM text of the C4 shape (rank 0's host) ----
+    path, text_bytes, text_docs = c4_corpus(args)
+    out = os.path.join(args.c4_dir, "out.bbmh")
+    threads = os.cpu_count() or 1
+    e2e = {}
+    l0 = bbmh.kernel_launches()
+    for name, sid, dim in (("4u-bit", 3, C4_DIM), ("2u", 1, C4_DIM_2U)):
+        fam = bbmh.Family(sid, dim, K, SEED)
+        fam.prepare(local)
+        fam.sketch_file(path, out, B, 10000, threads)  # warm: page cache, pinned pools
+        runs = []
+        for _ in range(args.e2e_steps or 3):
+            t = time.perf_counter()
+            st = fam.sketch_file(path, out, B, 10000, threads)
+            wall = time.perf_counter() - t
+            prof = bbmh.last_pipeline_profile()
+            runs.append((wall, st, prof))
+        wall, st, prof = min(runs, key=lambda r: r[0])
+        ev = text_docs * C4_NNZ * K
+        e2e[name] = {"value": ev / wall, "unit": "hash-evals/s", "wall_s": wall,
+                     "text_GBps": text_bytes / wall / 1e9, "docs_per_sec": text_docs / wall,
+                     "profile": prof, "stats": st,
+                     "hash_over_load": prof["hash_seconds"] / max(prof["load_seconds"], 1e-9),
+                     "hash_over_wall": prof["hash_seconds"] / wall,
+                     "runs_wall_s": [r[0] for r in runs]}
+        if name == "4u-bit":
+            # the same run with the text evicted from the page cache first: the
+            # load then includes the disk read
+            try:
+                fd = os.open(path, os.O_RDONLY)
+                os.fsync(fd)
+                os.posix_fadvise(fd, 0, 0, os.POSIX_FADV_DONTNEED)
+                os.close(fd)
+                t = time.perf_counter()
+                st = fam.sketch_file(path, out, B, 10000, threads)
+                cw = time.perf_counter() - t
+                cp = bbmh.last_pipeline_profile()
+                e2e[name]["cold_cache"] = {"wall_s": cw, "text_GBps": text_bytes / cw / 1e9,
+                                           "profile": cp,
+                                           "hash_over_load": cp["hash_seconds"] / max(cp["load_seconds"], 1e-9)}
+            except OSError as ex:
+                e2e[name]["cold_cache"] = {"error": str(ex)}
+            ours_records = open(out, "rb").read()[36:]
+        fam.close()
+        log(f"[c4 e2e {name}] {e2e[name]['wall_s']:.2f}s {e2e[name]['text_GBps']:.1f} GB/s of text, "
+            f"hash/load {e2e[name]['hash_over_load']:.2f}")
+    e2e_launches = bbmh.kernel_launches() - l0
+
+    # ---- CPU baseline: the reference's bbmh_sketch_file on a prefix of the text ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = c4_reference_sample(args, path, ours_records, cb)
+    head = kern["4u-bit"]
+    scale = C4_DOCS / text_docs
+    line = {
+        "metric": "hash_evals_per_sec", "value": head["hash_evals_per_sec"], "unit": "hash-evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (uniform sorted ids; device-generated CSR for value, LibSVM text "
+                "generated on this host for e2e)",
+        "config": {"workload": "rcv1-expanded shape C4: 677,399 docs x 12,000 nnz, 4U-bit "
+                               "D=1,010,017,424 (2U: D=2^30), k=500, b=8",
+                   "docs_per_gpu": n, "nnz_per_doc": C4_NNZ, "k": K, "b": B, "dim_4u": C4_DIM,
+                   "dim_2u": C4_DIM_2U, "parallelism": f"doc-sharded x{world}",
+                   "text_docs": text_docs, "text_bytes": text_bytes,
+                   "l2": "inputs (32.5 GB CSR / 20+ GB text) exceed L2; no flush needed"},
+        "docs_per_sec": head["docs_per_sec"],
+        "roofline": head["roofline"],
+        "schemes": kern,
+        "e2e": {"value": e2e["4u-bit"]["value"], "unit": "hash-evals/s",
+                "h2d_bytes_per_step": text_bytes, "d2h_bytes_per_step": text_docs * (cb + 1),
+                "api": "bbmh_sketch_file (LibSVM text -> BBMH, page-cache-resident text)",
+                "schemes": e2e,
+                "extrapolated_677399_docs_s": {k_: v["wall_s"] * scale for k_, v in e2e.items()},
+                "extrapolated": f"wall seconds x {C4_DOCS}/{text_docs} (same row shape, linear)"},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "gpu_launches": launches_kernel + e2e_launches,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def c4_reference_sample(args, path, ours_records, cb):
+    """The unmodified reference's bbmh_sketch_file (4U-bit) on the first
+    args.c4_ref_docs lines on all host threads; parity with our file's first
+    records; the rate is extrapolated (cost per document is size-independent)."""
+    from oracle import oracle as O
+    if not O.ref_available():
+        return None
+    R = O.ref()
+    threads = os.cpu_count() or 1
+    m = args.c4_ref_docs
+    pre = c4_prefix(path, m, os.path.join(args.c4_dir, f"prefix_{m}.txt"))
+    st, h = R.family(3, C4_DIM, K, SEED)
+    t = time.perf_counter()
+    s, stats = R.sketch_file(h, pre, os.path.join(args.c4_dir, "ref.bbmh"), B, 10000, threads, False)
+    secs = time.perf_counter() - t
+    R.destroy(h)
+    if s != 0:
+        return {"error": R.last_error()}
+    ref_records = open(os.path.join(args.c4_dir, "ref.bbmh"), "rb").read()[36:]
+    parity = ref_records == ours_records[: len(ref_records)] and len(ref_records) == m * (2 + cb)
+    return {"value": m * C4_NNZ * K / secs, "unit": "hash-evals/s", "cores": threads,
+            "kind": "reference", "parity_vs_gpu": parity, "extrapolated": True,
+            "text_GBps": os.path.getsize(pre) / secs / 1e9,
+            "read_s": stats.read_seconds, "compute_s": stats.compute_seconds, "wall_s": secs,
+            "sample": f"bbmh_sketch_file (4U-bit) on the first {m} docs of the C4 text, "
+                      f"workers={threads}; rate extrapolated to the full workload",
+            **host_info()}
+
+
+def run_c4_reference(args):
+    """`--impl reference --config c4`: the reference's bbmh_sketch_file on a
+    bounded prefix of the C4 text, per step."""
+    path, text_bytes, text_docs = c4_corpus(args)
+    from oracle import oracle as O
+    R = O.ref()
+    threads = os.cpu_count() or 1
+    m = args.c4_ref_docs
+    pre = c4_prefix(path, m, os.path.join(args.c4_dir, f"prefix_{m}.txt"))
+    st, h = R.family(3, C4_DIM, K, SEED)
+    secs = []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        s, _ = R.sketch_file(h, pre, os.path.join(args.c4_dir, "ref.bbmh"), B, 10000, threads, False)
+        if i >= args.warmup:
+            secs.append(time.perf_counter() - t)
+    R.destroy(h)
+    t = float(np.mean(secs))
+    v = m * C4_NNZ * K / t
+    print(json.dumps({
+        "impl": "reference", "metric": "hash_evals_per_sec", "value": v, "unit": "hash-evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic LibSVM text (tools/gen_libsvm.cpp)",
+        "config": {"workload": "rcv1-expanded shape C4 (4U-bit, k=500, b=8)", "reference_sample_docs": m,
+                   "extrapolated": True},
+        "cpu_baseline": {"value": v, "unit": "hash-evals/s", "cores": threads, "kind": "reference",
+                         "extrapolated": True,
+                         "sample": f"bbmh_sketch_file on the first {m} of {text_docs} docs per step",
+                         **host_info()},
+        "e2e": {"value": v, "unit": "hash-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c4"])
     ap.add_argument("--docs", type=int, default=N_DOCS)
-    ap.add_argument("--schemes", default="2u,4u-bit,4u-mod")
+    ap.add_argument("--schemes", default="2u,4u-bit,4u-mod,perm")
+    ap.add_argument("--perm-steps", type=int, default=3)
     ap.add_argument("--scheme", default="2u", help="reference arm scheme")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0: --steps")
     ap.add_argument("--ref-docs", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--c4-docs", type=int, default=C4_DOCS, help="device-resident C4 corpus")
+    ap.add_argument("--c4-text-docs", type=int, default=150_000, help="C4 LibSVM text (~143 KB/doc)")
+    ap.add_argument("--c4-ref-docs", type=int, default=1500)
+    ap.add_argument("--c4-dir", default="/tmp/bbmh_c4")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

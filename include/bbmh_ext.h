@@ -122,6 +122,31 @@ BBMH_API bbmh_status bbmh_ext_set_option(const char* name, int64_t value);
 BBMH_API bbmh_status bbmh_ext_get_option(const char* name, int64_t* value_out);
 BBMH_API const char* bbmh_ext_option_name(uint32_t i);
 
+/* The host-bandwidth budget that picks the id transfer of the host-buffer
+ * paths when `feeds` GPUs stream ids from this host at once (lanes x the
+ * "host_sharers" option): ids/s with 4-byte ids (link and DRAM bound) and
+ * with 16-bit differences (link and measured host-encode bound), and whether
+ * the encoded form is used. Measures the host on first use (~0.3 s). */
+BBMH_API bbmh_status bbmh_ext_host_budget(uint32_t feeds, double* raw_ids_per_s,
+                                          double* encoded_ids_per_s, int32_t* encoded_pays);
+
+/* Stage breakdown of the calling thread's last bbmh_sketch_file /
+ * bbmh_ext_predict_corpus call. Seconds are summed over lanes (one lane per
+ * GPU) except wall_seconds. */
+typedef struct bbmh_ext_pipeline_profile {
+    double wall_seconds;
+    double io_seconds;     /* pread of the input, summed over waiting threads */
+    double parse_seconds;  /* LibSVM parse calls (GPU parser incl. its text H2D, or CPU rounds) */
+    double load_seconds;   /* loader threads busy producing batches (read + parse) */
+    double hash_seconds;   /* sketch kernels, device time */
+    double write_seconds;  /* in-order writer */
+    uint64_t input_bytes;
+    uint64_t records;
+    uint64_t lanes;        /* GPUs (lanes) that sketched */
+    uint64_t ranges;       /* line-aligned text ranges (range-sharded loaders); 0 = one reader */
+} bbmh_ext_pipeline_profile;
+BBMH_API bbmh_status bbmh_ext_last_pipeline_profile(bbmh_ext_pipeline_profile* out);
+
 /* Monotonic per-process counters of which routes ran: "kernel_launches",
  * "h2d_bytes", "d2h_bytes", "peer_copy_bytes", "zero_copy_calls",
  * "delta16_chunks", "raw_chunks", "range_shards", "device_id_batches". */

@@ -48,6 +48,17 @@ class PipelineStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class PipelineProfile(C.Structure):
+    _fields_ = [("wall_seconds", C.c_double), ("io_seconds", C.c_double),
+                ("parse_seconds", C.c_double), ("load_seconds", C.c_double),
+                ("hash_seconds", C.c_double), ("write_seconds", C.c_double),
+                ("input_bytes", C.c_uint64), ("records", C.c_uint64), ("lanes", C.c_uint64),
+                ("ranges", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class BbmhError(RuntimeError):
     def __init__(self, status: int, message: str):
         super().__init__(f"bbmh status {status}: {message}")
@@ -104,6 +115,9 @@ def lib() -> C.CDLL:
         "bbmh_ext_get_option": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int32),
         "bbmh_ext_option_name": ([C.c_uint32], C.c_char_p),
         "bbmh_ext_counter": ([C.c_char_p, u64p], C.c_int32),
+        "bbmh_ext_last_pipeline_profile": ([C.POINTER(PipelineProfile)], C.c_int32),
+        "bbmh_ext_host_budget": ([C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double), i32p],
+                                 C.c_int32),
         "bbmh_ext_family_perm_table": ([C.c_void_p, C.c_uint32, u32p], C.c_int32),
     }
     for name, (args, res) in sig.items():
@@ -330,6 +344,21 @@ class option:
     def __exit__(self, *a):
         for k, v in self.old.items():
             set_option(k, v)
+
+
+def host_budget(feeds: int = 1) -> dict:
+    """bbmh_ext_host_budget: the id-transfer budget for `feeds` GPUs on this host."""
+    raw, enc, pays = C.c_double(0), C.c_double(0), C.c_int32(0)
+    _check(lib().bbmh_ext_host_budget(feeds, C.byref(raw), C.byref(enc), C.byref(pays)))
+    return {"feeds": feeds, "raw_ids_per_s": raw.value, "encoded_ids_per_s": enc.value,
+            "encoded": bool(pays.value)}
+
+
+def last_pipeline_profile() -> dict:
+    """bbmh_ext_last_pipeline_profile: stage seconds of this thread's last file pipeline."""
+    p = PipelineProfile()
+    _check(lib().bbmh_ext_last_pipeline_profile(C.byref(p)))
+    return p.as_dict()
 
 
 def counter(name: str) -> int:

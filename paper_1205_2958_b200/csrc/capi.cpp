@@ -323,6 +323,26 @@ bbmh_status bbmh_ext_get_option(const char* name, int64_t* value_out) {
 
 const char* bbmh_ext_option_name(uint32_t i) { return opt_name(int(i)); }
 
+bbmh_status bbmh_ext_last_pipeline_profile(bbmh_ext_pipeline_profile* out) {
+    return guarded([&] {
+        if (!out) fail(Errc::InvalidArgument, "out must not be NULL");
+        const PipelineProfile p = last_pipeline_profile();
+        *out = {p.wall_seconds,  p.io_seconds,  p.parse_seconds, p.load_seconds, p.hash_seconds,
+                p.write_seconds, p.input_bytes, p.records,       p.lanes,        p.ranges};
+    });
+}
+
+bbmh_status bbmh_ext_host_budget(uint32_t feeds, double* raw_ids_per_s, double* encoded_ids_per_s,
+                                 int32_t* encoded_pays) {
+    return guarded([&] {
+        double raw = 0, enc = 0;
+        const bool pays = delta16_budget_pays(feeds, &raw, &enc);
+        if (raw_ids_per_s) *raw_ids_per_s = raw;
+        if (encoded_ids_per_s) *encoded_ids_per_s = enc;
+        if (encoded_pays) *encoded_pays = pays ? 1 : 0;
+    });
+}
+
 bbmh_status bbmh_ext_counter(const char* name, uint64_t* value_out) {
     return guarded([&] {
         require(name, "name");

@@ -46,6 +46,21 @@ private:
 
 [[noreturn]] inline void fail(Errc code, std::string msg) { throw Error(code, std::move(msg)); }
 
+// A parse error at a (1-based) line of the text: the message is the
+// reference's "line N: <detail>" (dataio.cpp:60-106). Range-sharded loaders
+// count lines per range and renumber with the lines of the ranges before.
+class LineError : public Error {
+public:
+    LineError(Errc code, uint64_t line, std::string detail)
+        : Error(code, "line " + std::to_string(line) + ": " + detail), line_(line), detail_(std::move(detail)) {}
+    uint64_t line() const { return line_; }
+    const std::string& detail() const { return detail_; }
+
+private:
+    uint64_t line_;
+    std::string detail_;
+};
+
 // Developer tracing: with the "trace" option on (options.hpp), prints
 // "bbmh-trace <ms since first call> <what>" to stderr (pipeline stage timing).
 void trace(const char* what);

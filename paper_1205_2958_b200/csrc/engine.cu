@@ -9,6 +9,7 @@
 // sharding, no collective): output position depends only on the chunk index.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -491,25 +492,58 @@ uint64_t chunk_idx_cap() {
     return v >= (1 << 16) ? uint64_t(v) : kChunkIdxCap;
 }
 
-// Host-encode rate of the 16-bit transfer, ids/s per host core (AVX2 encode
-// with streaming stores, profiles/r11/host_encode_probe.jsonl: ~4.5 GB/s of ids).
-constexpr double kEncodeIdsPerCore = 1.1e9;
-
 }  // namespace
+
+// Ids/s the host encodes on all its cores (the shipped encoder on a
+// webspam-shaped 32 Mi-id chunk, larger than the host's L3; best of 3),
+// measured once per process. This rate includes the encode's own DRAM
+// traffic (4 B read + 2 B written per id).
+double host_encode_ids_per_s() {
+    static const double rate = [] {
+        constexpr uint64_t kRows = 8192, kPerRow = 4096, kIds = kRows * kPerRow;
+        std::vector<uint64_t> rp(kRows + 1);
+        std::vector<uint32_t> ids(kIds);
+        std::vector<uint16_t> deltas(kIds);
+        std::vector<uint32_t> exc_ptr(kRows + 1), exc(kIds / 8 + 64);
+        for (uint64_t r = 0; r <= kRows; ++r) rp[r] = r * kPerRow;
+        host_parallel(host_threads(), [&](unsigned w) {
+            const uint64_t T = host_threads(), lo = kRows * w / T, hi = kRows * (w + 1) / T;
+            for (uint64_t r = lo; r < hi; ++r) {
+                uint32_t v = uint32_t(mix64(r) & 1023);
+                for (uint64_t i = 0; i < kPerRow; ++i) {
+                    v += 1 + uint32_t(mix64(r * kPerRow + i) % 8191);  // mean gap ~4,096
+                    ids[r * kPerRow + i] = v;
+                }
+            }
+        });
+        double best = 0;
+        for (int rep = 0; rep < 3; ++rep) {
+            uint64_t nexc = 0;
+            const auto t0 = std::chrono::steady_clock::now();
+            encode_delta16(rp.data(), kRows, 0, ids.data(), deltas.data(), exc_ptr.data(), exc.data(),
+                           exc.size(), nexc);
+            const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            best = std::max(best, double(kIds) / s);
+        }
+        return best;
+    }();
+    return rate;
+}
 
 // Host bandwidth budget of the id transfer when `feeds` GPUs stream ids from
 // this host at once (lanes of this process x "host_sharers", e.g. the ranks
-// of one node). Per id, 4-byte ids cost 4 B of link and 4 B of DRAM reads
-// (the DMA); 2-byte ids cost 2 B of link, 8 B of DRAM traffic (the encode
-// reads 4 and writes 2, the DMA reads 2) and host-core time. The encode pays
-// when it moves more ids per second than the raw copy.
+// of one node). 4-byte ids cost 4 B of link per id and 4 B of DRAM reads
+// (the DMA): min(feeds x link / 4, DRAM / 4) ids/s. 2-byte ids cost 2 B of
+// link, but every id is first encoded by the host cores, which all feeds
+// share: min(feeds x link / 2, the host's measured encode rate). The encode
+// pays when it moves more ids per second (on a 16-core B200 host with one
+// GPU: ~17 G against ~14 G ids/s; with two GPUs the raw copy wins).
 bool delta16_budget_pays(uint64_t feeds, double* raw_ids_s, double* enc_ids_s) {
     feeds = std::max<uint64_t>(1, feeds);
     const double link = double(std::max<int64_t>(1, opt(Opt::PcieGbs))) * 1e9;
     const double dram = host_dram_bytes_per_s();
-    const double cores = double(host_threads()) / double(feeds);  // cores per feed
     const double raw = std::min(double(feeds) * link / 4, dram / 4);
-    const double enc = std::min({double(feeds) * link / 2, dram / 8, double(feeds) * cores * kEncodeIdsPerCore});
+    const double enc = std::min(double(feeds) * link / 2, host_encode_ids_per_s());
     if (raw_ids_s) *raw_ids_s = raw;
     if (enc_ids_s) *enc_ids_s = enc;
     return enc > 1.05 * raw;

@@ -38,6 +38,7 @@ void copy_perm_table(const Family& f, uint32_t j, uint32_t* out);
 // Whether 16-bit id transfer moves more ids/s than 4-byte ids when `feeds`
 // GPUs stream from this host (engine.cu); the two rates are returned too.
 bool delta16_budget_pays(uint64_t feeds, double* raw_ids_s, double* enc_ids_s);
+double host_encode_ids_per_s();
 
 // Devices used by the host-buffer and file pipelines (empty = current device).
 std::vector<int> pipeline_devices();

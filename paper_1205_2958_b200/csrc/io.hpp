@@ -64,6 +64,12 @@ public:
     // The GPU that parses this corpus (-1: none): batches filled with
     // want_device_ids get their ids there.
     virtual int parser_device() const { return -1; }
+    // Lines of text consumed so far (blank ones included; 0 for binary input).
+    virtual uint64_t lines_consumed() const { return 0; }
+    // Seconds spent reading the file (pread, summed over the threads that
+    // wait for it) and parsing blocks (GPU parser calls, CPU parser rounds).
+    virtual double io_seconds() const { return 0; }
+    virtual double parse_seconds() const { return 0; }
 };
 
 // open_corpus: sniff the "BBCV" magic, else LibSVM text (dataio.cpp:257-264).
@@ -71,6 +77,24 @@ public:
 // row source, learner.cpp:236-256).
 std::unique_ptr<CorpusReader> open_corpus(const std::string& path, unsigned parse_threads,
                                           bool libsvm_values = false);
+
+// True if `path` is LibSVM text (no BBCV magic).
+bool is_libsvm_text(const std::string& path);
+
+// Byte size of a file.
+uint64_t file_size(const std::string& path);
+
+// The offset of the first line that starts at or after `off` (0 stays 0;
+// the size of the file if no line starts there): the cut points of
+// range-sharded text, so every range holds whole lines.
+uint64_t line_start_at_or_after(const std::string& path, uint64_t off);
+
+// LibSVM text (binary mode, the sketch loader) restricted to the whole lines
+// in [begin, end) -- begin and end are line starts or the end of the file.
+// Line numbers in its errors count from the range's first line (1-based).
+// The GPU parser, if used, runs on the current device.
+std::unique_ptr<CorpusReader> open_libsvm_range(const std::string& path, unsigned parse_threads,
+                                                uint64_t begin, uint64_t end);
 
 // BBMH sketch file reader (SketchReader, sketch.cpp:143-207): header checks
 // with the reference's messages, then records in batches (label, flags,

@@ -230,7 +230,9 @@ struct Item {
 // the producer: it issues one TMA bulk copy per item into one of two shared
 // buffers (completion signalled on an mbarrier) one item ahead, so the next
 // document's ids land while the current one is hashed.
-template <int SCHEME, bool POW2, int J>
+// TRACE (tools/residency_probe.cu only): thread 0 of every CTA records its
+// SM, start and end times (%globaltimer, ns) and the documents it finished.
+template <int SCHEME, bool POW2, int J, bool TRACE = false>
 __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint64_t* __restrict__ row_ptr,
                                                      uint64_t index_base,
                                                      const uint32_t* __restrict__ indices,
@@ -238,7 +240,8 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
                                                      uint32_t tile,
                                                      uint8_t* __restrict__ codes,
                                                      uint64_t* __restrict__ minima,
-                                                     uint8_t* __restrict__ flags, int* err) {
+                                                     uint8_t* __restrict__ flags, int* err,
+                                                     unsigned long long* cta_trace = nullptr) {
     extern __shared__ __align__(128) uint32_t smem[];
     const uint32_t kBuf = tile + 8;
     uint32_t* s_code = smem + 2 * kBuf;  // jtile codes
@@ -249,6 +252,9 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
     const uint32_t tpb = blockDim.x;
     const uint32_t k = F.k;
     const uint32_t j0 = blockIdx.y * jtile;
+    [[maybe_unused]] unsigned long long trace_t0 = 0;
+    [[maybe_unused]] uint32_t trace_docs = 0;
+    if constexpr (TRACE) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
     const uint32_t jcnt = min(jtile, k - j0);
 
     // ---- producer state (thread 0 only) ----
@@ -374,6 +380,7 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         }
         if (d.last) {
             // ---- epilogue: minima -> codes -> packed bitstream (sketch.cpp:80-98) ----
+            if constexpr (TRACE) ++trace_docs;
             const uint64_t doc = d.doc;
             const bool empty = d.empty;
 #pragma unroll
@@ -407,6 +414,19 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
             }
         }
         __syncthreads();  // buffer bi and s_code free; desc[bi ^ 1] visible
+    }
+    if constexpr (TRACE) {
+        if (tid == 0) {
+            unsigned long long t1;
+            uint32_t smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            unsigned long long* o = cta_trace + 4 * ((uint64_t)blockIdx.y * gridDim.x + blockIdx.x);
+            o[0] = smid;
+            o[1] = trace_t0;
+            o[2] = t1;
+            o[3] = trace_docs;
+        }
     }
 }
 
@@ -535,11 +555,12 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
     }
 }
 
-template <int SCHEME, bool POW2, int J>
+template <int SCHEME, bool POW2, int J, bool TRACE = false>
 void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* row_ptr,
                 uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
-                uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
-    auto kern = sketch_kernel<SCHEME, POW2, J>;
+                uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st,
+                unsigned long long* cta_trace = nullptr) {
+    auto kern = sketch_kernel<SCHEME, POW2, J, TRACE>;
     // 1,024-id tiles for 2U and for 4U below 256 threads per CTA: 4U CTAs of one
     // or two warps with 4,096-id tiles are held to ~7 per SM by shared memory
     // (k = 32: 0.91 -> 1.25 T evals/s, k = 64: 0.95 -> 1.31; tools/grid_4u_tiles.json)
@@ -601,7 +622,7 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     dim3 grid((unsigned)gx, sh.jtiles);
     const cudaError_t pre = cudaPeekAtLastError();
     kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr, base, idx, n, b, sh.jtile, (uint32_t)tile, codes,
-                                     minima, flags, err);
+                                     minima, flags, err, cta_trace);
     if (const cudaError_t e = cudaPeekAtLastError(); e != cudaSuccess)
         fprintf(stderr, "bbmh: sketch launch failed (%s; before launch: %s) grid %u x %u tpb %d smem %zu\n",
                 cudaGetErrorString(e), cudaGetErrorString(pre), grid.x, grid.y, sh.tpb, smem);

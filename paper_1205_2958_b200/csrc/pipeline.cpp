@@ -13,9 +13,11 @@
 #include <cstdlib>
 #include <condition_variable>
 #include <cstring>
+#include <atomic>
 #include <deque>
 #include <exception>
 #include <map>
+#include <utility>
 #include <mutex>
 #include <thread>
 
@@ -33,6 +35,8 @@ double since(Clock::time_point t0) {
 }
 
 constexpr uint64_t kBatchIds = 1ull << 24;  // ids per loader batch (64 MiB pinned)
+
+thread_local PipelineProfile t_profile;
 
 template <typename T>
 class BlockingQueue {
@@ -322,25 +326,310 @@ PipelineStats run_stream(const Family& f, CorpusReader& reader, uint8_t b, bool 
     trace("stream: joined");
     if (error) std::rethrow_exception(error);
     for (double ms : kernel_ms) stats.compute_seconds += ms * 1e-3;
+    PipelineProfile& pr = t_profile;
+    pr.io_seconds = reader.io_seconds();
+    pr.parse_seconds = reader.parse_seconds();
+    pr.load_seconds = stats.read_seconds;
+    pr.hash_seconds = stats.compute_seconds;
+    pr.write_seconds = stats.write_seconds;
+    pr.records = stats.records;
+    pr.lanes = devs.size();
+    pr.ranges = 0;
     return stats;
 }
 
+// order-restoring buffer over (range, batch) keys: range r's batches come
+// before range r+1's; a range's batch count is known when its loader is done
+class RangeReorder {
+public:
+    using Key = std::pair<uint64_t, uint64_t>;
+    void put(Key key, OutBatch&& b) {
+        std::lock_guard lk(m_);
+        done_[key] = std::move(b);
+        cv_.notify_all();
+    }
+    void set_range_total(uint64_t r, uint64_t total) {
+        std::lock_guard lk(m_);
+        totals_[r] = total;
+        cv_.notify_all();
+    }
+    // false at the end of range r (or on abort)
+    bool take(Key key, OutBatch& out) {
+        std::unique_lock lk(m_);
+        cv_.wait(lk, [&] {
+            if (aborted_ || done_.count(key)) return true;
+            auto t = totals_.find(key.first);
+            return t != totals_.end() && key.second >= t->second;
+        });
+        if (aborted_) return false;
+        auto it = done_.find(key);
+        if (it == done_.end()) return false;
+        out = std::move(it->second);
+        done_.erase(it);
+        return true;
+    }
+    void abort() {
+        std::lock_guard lk(m_);
+        aborted_ = true;
+        cv_.notify_all();
+    }
+
+private:
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::map<Key, OutBatch> done_;
+    std::map<uint64_t, uint64_t> totals_;
+    bool aborted_ = false;
+};
+
+// Range-sharded LibSVM text (several GPUs sketching one text file): the file
+// is cut at line starts into `lanes * range_shards` byte ranges. Every lane
+// has its own loader thread, which claims ranges in order and reads, parses
+// (on the lane's own GPU, ids left there) and batches them; its lane thread
+// sketches them. Nothing goes back through the host or another GPU, and no
+// single reader or parser bounds the file. The calling thread writes range 0's
+// batches, then range 1's, ... so the bytes equal the one-reader pipeline's
+// (pipeline.cpp:76-119 ordering). A parse error is reported as the reference
+// reports it -- the first bad line in file order, numbered from the start of
+// the file: a range's error is raised when the writer reaches it, after every
+// earlier range has been written and counted.
+template <typename Append>
+PipelineStats run_ranged(const Family& f, const std::string& path, unsigned threads, uint8_t b,
+                         bool emit_minima, const ScoreModel* score, Append&& append) {
+    trace("ranged: start");
+    PipelineStats stats;
+    const size_t cb = packed_code_bytes(f.k, b);
+    const std::vector<int> devs = pipeline_devices();
+    const uint64_t max_docs = chunk_docs_setting();
+    const bool b_ok = b >= 1 && b <= 32;
+    const uint64_t size = file_size(path);
+    const uint64_t nr = std::max<uint64_t>(1, devs.size() * uint64_t(std::max<int64_t>(1, opt(Opt::RangeShards))));
+    std::vector<uint64_t> cut(nr + 1, size);
+    cut[0] = 0;
+    for (uint64_t r = 1; r < nr; ++r)
+        cut[r] = std::max(cut[r - 1], line_start_at_or_after(path, size / nr * r));
+
+    struct RangeErr {
+        Errc code = Errc::Io;
+        uint64_t line = 0;
+        std::string detail;
+        bool set = false;
+    };
+    std::vector<RangeErr> range_err(nr);
+    std::vector<uint64_t> range_lines(nr, 0);
+    std::atomic<uint64_t> next_range{0}, err_range{UINT64_MAX}, records{0};
+    std::atomic<uint64_t> io_ns{0}, parse_ns{0}, load_ns{0};
+    RangeReorder done;
+    std::mutex err_mu;
+    std::exception_ptr error;
+    struct LaneQueues {
+        BlockingQueue<Batch*> free_q, in_q;
+    };
+    std::vector<std::unique_ptr<LaneQueues>> qs;
+    for (size_t i = 0; i < devs.size(); ++i) qs.push_back(std::make_unique<LaneQueues>());
+    auto record_error = [&](std::exception_ptr e) {
+        {
+            std::lock_guard lk(err_mu);
+            if (!error) error = e;
+        }
+        for (auto& q : qs) {
+            q->free_q.abort();
+            q->in_q.abort();
+        }
+        done.abort();
+    };
+    const size_t per_lane = 4;
+    BatchLease storage(per_lane * devs.size());
+    for (size_t i = 0; i < storage.batches.size(); ++i) qs[i / per_lane]->free_q.push(storage.batches[i]);
+    auto ns_since = [](Clock::time_point t0) {
+        return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
+    };
+
+    std::vector<std::thread> loaders, lanes;
+    for (size_t di = 0; di < devs.size(); ++di) {
+        loaders.emplace_back([&, di] {
+            LaneQueues& q = *qs[di];
+            try {
+                BBMH_CUDA(cudaSetDevice(devs[di]));
+                for (uint64_t r; (r = next_range.fetch_add(1)) < nr;) {
+                    if (r > err_range.load()) break;  // an earlier range failed: the rest is moot
+                    count(Counter::RangeShards);
+                    uint64_t seq = 0;
+                    auto reader = open_libsvm_range(path, threads, cut[r], cut[r + 1]);
+                    const bool device_ids = reader->parser_device() == devs[di] && opt(Opt::DeviceIds);
+                    try {
+                        for (;;) {
+                            Batch* bt = nullptr;
+                            if (!q.free_q.pop(bt)) return;
+                            const auto t0 = Clock::now();
+                            bt->clear();
+                            bt->want_device_ids = device_ids;
+                            if (!device_ids) bt->reserve_ids(kBatchIds + kBatchIds / 4);
+                            bool got = false;
+                            try {
+                                got = reader->fill(*bt, max_docs, kBatchIds);
+                            } catch (...) {
+                                q.free_q.push(bt);
+                                throw;
+                            }
+                            load_ns += ns_since(t0);
+                            if (!got) {
+                                q.free_q.push(bt);
+                                break;
+                            }
+                            if (!b_ok) fail(Errc::InvalidArgument, "b must be in 1..32");  // sketch.cpp:73
+                            bt->seq = r;
+                            bt->first_record = seq++;  // (range, batch) key of this batch
+                            records += bt->n;
+                            if (bt->want_device_ids && bt->d_dev == devs[di] && bt->d_valid == bt->nids())
+                                count(Counter::DeviceIdBatches);
+                            q.in_q.push(bt);
+                            if (r > err_range.load()) break;
+                        }
+                    } catch (const LineError& e) {
+                        std::lock_guard lk(err_mu);
+                        range_err[r] = {e.code(), e.line(), e.detail(), true};
+                        uint64_t cur = err_range.load();
+                        while (r < cur && !err_range.compare_exchange_weak(cur, r)) {
+                        }
+                    }
+                    range_lines[r] = reader->lines_consumed();
+                    io_ns += uint64_t(reader->io_seconds() * 1e9);
+                    parse_ns += uint64_t(reader->parse_seconds() * 1e9);
+                    done.set_range_total(r, seq);
+                }
+                q.in_q.close();
+            } catch (...) {
+                record_error(std::current_exception());
+            }
+        });
+    }
+    std::vector<double> kernel_ms(devs.size(), 0.0);
+    for (size_t di = 0; di < devs.size(); ++di) {
+        lanes.emplace_back([&, di] {
+            LaneQueues& q = *qs[di];
+            try {
+                BBMH_CUDA(cudaSetDevice(devs[di]));
+                Lane lane(f, devs[di], b_ok ? b : 8, emit_minima, score);
+                std::map<uint64_t, Batch*> inflight;
+                uint64_t tag = 0;
+                auto on_done = [&](const ChunkResult& res) {
+                    Batch* bt = inflight.at(res.tag);
+                    inflight.erase(res.tag);
+                    OutBatch ob;
+                    ob.n = res.n;
+                    ob.recs.resize(res.n * (2 + cb));
+                    uint8_t* p = ob.recs.data();
+                    for (uint64_t i = 0; i < res.n; ++i, p += 2 + cb) {
+                        p[0] = uint8_t(bt->labels[i]);
+                        p[1] = res.flags[i];
+                        std::memcpy(p + 2, res.codes + i * cb, cb);
+                    }
+                    if (emit_minima) ob.minima.assign(res.minima, res.minima + res.n * f.k);
+                    if (res.scores) ob.scores.assign(res.scores, res.scores + res.n);
+                    kernel_ms[di] += res.kernel_ms;
+                    const RangeReorder::Key key{bt->seq, bt->first_record};
+                    q.free_q.push(bt);
+                    done.put(key, std::move(ob));
+                };
+                Batch* bt = nullptr;
+                while (q.in_q.pop(bt)) {
+                    ChunkJob job;
+                    job.tag = tag;
+                    job.row_ptr = bt->row_ptr.data();
+                    job.index_base = 0;
+                    job.indices = bt->ids;
+                    job.n = bt->n;
+                    job.pinned_input = true;
+                    if (bt->want_device_ids && bt->d_dev == devs[di] && bt->d_valid == bt->nids())
+                        job.d_indices = bt->d_ids;
+                    inflight[tag++] = bt;
+                    lane.submit(job, on_done);
+                }
+                lane.drain(on_done);
+            } catch (...) {
+                record_error(std::current_exception());
+            }
+        });
+    }
+
+    // the calling thread writes the ranges in file order
+    try {
+        uint64_t lines_before = 0;
+        for (uint64_t r = 0; r < nr; ++r) {
+            OutBatch ob;
+            for (uint64_t s = 0; done.take({r, s}, ob); ++s) {
+                const auto t0 = Clock::now();
+                append(ob);
+                stats.write_seconds += since(t0);
+            }
+            {
+                std::lock_guard lk(err_mu);
+                if (error) break;
+            }
+            if (range_err[r].set) {
+                const RangeErr& e = range_err[r];
+                throw LineError(e.code, lines_before + e.line, e.detail);
+            }
+            lines_before += range_lines[r];
+        }
+    } catch (...) {
+        record_error(std::current_exception());
+    }
+    for (auto& t : loaders) t.join();
+    for (auto& t : lanes) t.join();
+    trace("ranged: joined");
+    if (error) std::rethrow_exception(error);
+    stats.records = records.load();
+    stats.read_seconds = double(load_ns.load()) * 1e-9;
+    for (double ms : kernel_ms) stats.compute_seconds += ms * 1e-3;
+    PipelineProfile& pr = t_profile;
+    pr.io_seconds = double(io_ns.load()) * 1e-9;
+    pr.parse_seconds = double(parse_ns.load()) * 1e-9;
+    pr.load_seconds = stats.read_seconds;
+    pr.hash_seconds = stats.compute_seconds;
+    pr.write_seconds = stats.write_seconds;
+    pr.records = stats.records;
+    pr.lanes = devs.size();
+    pr.ranges = nr;
+    return stats;
+}
+
+// Several GPUs on one LibSVM text file read it as line-aligned ranges, one
+// loader per GPU (run_ranged); "range_shards" > 1 does so on one GPU too.
+bool use_ranges(const std::string& path) {
+    const int64_t rs = opt(Opt::RangeShards);
+    if (rs <= 0) return false;
+    return (pipeline_devices().size() > 1 || rs > 1) && is_libsvm_text(path);
+}
+
 }  // namespace
+
+PipelineProfile last_pipeline_profile() { return t_profile; }
 
 PipelineStats sketch_file(const Family& f, const std::string& input_path,
                           const std::string& output_path, uint8_t b, uint64_t chunk_size,
                           uint32_t workers, bool emit_minima) {
     const auto wall0 = Clock::now();
+    t_profile = PipelineProfile{};
     // open order as in sketch_file (pipeline.cpp:217-220) and sketch_stream (:125-126)
     auto reader = open_corpus(input_path, workers ? workers : 1);
     SketchWriter writer(output_path, f, b, emit_minima);
     if (chunk_size < 1) fail(Errc::InvalidArgument, "chunk_size must be >= 1");
     if (workers < 1) fail(Errc::InvalidArgument, "workers must be >= 1");
-    PipelineStats stats = run_stream(f, *reader, b, emit_minima, nullptr,
-                                     [&](const OutBatch& ob) { writer.append(ob); });
+    auto sink = [&](const OutBatch& ob) { writer.append(ob); };
+    PipelineStats stats;
+    if (use_ranges(input_path)) {
+        reader.reset();  // each lane opens its own ranges
+        stats = run_ranged(f, input_path, workers, b, emit_minima, nullptr, sink);
+    } else {
+        stats = run_stream(f, *reader, b, emit_minima, nullptr, sink);
+    }
     writer.close();
     stats.chunks = (stats.records + chunk_size - 1) / chunk_size;  // reference chunking
     stats.wall_seconds = since(wall0);
+    t_profile.wall_seconds = stats.wall_seconds;
+    t_profile.input_bytes = file_size(input_path);
     return stats;
 }
 

@@ -20,6 +20,23 @@ struct PipelineStats {
     double wall_seconds = 0;
 };
 
+// Stage breakdown of the calling thread's last file pipeline
+// (bbmh_ext_last_pipeline_profile). Seconds are summed over lanes except
+// wall_seconds; per-lane figures divide by `lanes`.
+struct PipelineProfile {
+    double wall_seconds = 0;
+    double io_seconds = 0;      // pread of the text / BBCV bytes (threads waiting on it)
+    double parse_seconds = 0;   // LibSVM parse calls (GPU parser incl. its H2D, or CPU rounds)
+    double load_seconds = 0;    // loader threads busy producing batches (read + parse)
+    double hash_seconds = 0;    // sketch kernels, device time
+    double write_seconds = 0;   // in-order writer
+    uint64_t input_bytes = 0;
+    uint64_t records = 0;
+    uint64_t lanes = 0;
+    uint64_t ranges = 0;        // text ranges (range-sharded loaders), 0 = one shared reader
+};
+PipelineProfile last_pipeline_profile();
+
 // sketch_file (pipeline.cpp:215-226): corpus -> BBMH sketch (+ .min64).
 PipelineStats sketch_file(const Family& f, const std::string& input_path,
                           const std::string& output_path, uint8_t b, uint64_t chunk_size,

@@ -9,7 +9,20 @@ the only collective is the final gather of the (small) codes to the writer.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
+
+
+def configure_host_sharing(local_world_size: int | None = None) -> int:
+    """Tell the library how many GPU feeds share this host's DRAM and cores
+    (the ranks of this job on this node: LOCAL_WORLD_SIZE under torchrun), so
+    its id-transfer budget (bbmh_ext_host_budget) counts them. Returns it."""
+    from . import bbmh
+    n = local_world_size or int(os.environ.get("LOCAL_WORLD_SIZE", "1") or 1)
+    n = max(1, n)
+    bbmh.set_option("host_sharers", n)
+    return n
 
 
 def shard_bounds(row_ptr: np.ndarray, world: int, row_cost: int = 64) -> list[tuple[int, int]]:

@@ -89,3 +89,39 @@ def test_local_rows_rebases():
     idx = np.arange(10, dtype=np.uint32)
     lrp, lidx = local_rows(rp, idx, 1, 3)
     assert list(lrp) == [0, 0, 4] and list(lidx) == [3, 4, 5, 6]
+
+
+def _budget_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")))
+    from paper_1205_2958_b200 import bbmh, shard
+    n = shard.configure_host_sharing()
+    # rates from fixed host figures so both ranks (and the assertion) agree
+    bbmh.set_option("host_dram_gbs", 150)
+    one, two = bbmh.host_budget(1), bbmh.host_budget(n)
+    q.put((rank, bbmh.get_option("host_sharers"), one, two))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_host_sharing_budget():
+    """Ranks of one node tell the library they share its host (LOCAL_WORLD_SIZE),
+    and the id-transfer budget counts both feeds: the raw copy's ids/s scale
+    with the links, the encoded form's are capped by the one host's encode rate."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_budget_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, sharers, one, two in got:
+        assert sharers == 2
+        assert two["raw_ids_per_s"] >= one["raw_ids_per_s"]
+        assert two["encoded_ids_per_s"] <= 2 * one["encoded_ids_per_s"] + 1
+        assert two["raw_ids_per_s"] <= 150e9 / 4 + 1
