@@ -692,11 +692,11 @@ def run_c4(args, torch, dev, rank, world, local, barrier, max_over_ranks, bbmh):
 
     # ---- e2e: bbmh_sketch_file on LibSVM text of the C4 shape (rank 0's host) ----
     path, text_bytes, text_docs = c4_corpus(args)
-    out = os.path.join(args.c4_dir, "out.bbmh")
     threads = os.cpu_count() or 1
     e2e = {}
     l0 = bbmh.kernel_launches()
     for name, sid, dim in (("4u-bit", 3, C4_DIM), ("2u", 1, C4_DIM_2U)):
+        out = os.path.join(args.c4_dir, f"out_{name}.bbmh")
         fam = bbmh.Family(sid, dim, K, SEED)
         fam.prepare(local)
         fam.sketch_file(path, out, B, 10000, threads)  # warm: page cache, pinned pools
@@ -736,6 +736,7 @@ def run_c4(args, torch, dev, rank, world, local, barrier, max_over_ranks, bbmh):
         fam.close()
         log(f"[c4 e2e {name}] {e2e[name]['wall_s']:.2f}s {e2e[name]['text_GBps']:.1f} GB/s of text, "
             f"hash/load {e2e[name]['hash_over_load']:.2f}")
+    replay = c4_replay(bbmh, path, os.path.join(args.c4_dir, "out_4u-bit.bbmh"), local, threads)
     e2e_launches = bbmh.kernel_launches() - l0
 
     # ---- CPU baseline: the reference's bbmh_sketch_file on a prefix of the text ----
@@ -765,11 +766,41 @@ def run_c4(args, torch, dev, rank, world, local, barrier, max_over_ranks, bbmh):
                 "schemes": e2e,
                 "extrapolated_677399_docs_s": {k_: v["wall_s"] * scale for k_, v in e2e.items()},
                 "extrapolated": f"wall seconds x {C4_DOCS}/{text_docs} (same row shape, linear)"},
+        "epoch_replay": replay,
         "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": launches_kernel + e2e_launches,
     }
     print(json.dumps(line), flush=True)
+
+
+def c4_replay(bbmh, text_path, sketch_path, device, threads, epochs=2):
+    """Paper Table 4 at the C4 shape: loading time per
+    epoch of the original LibSVM text (parsed on the GPU, rows as device CSR)
+    against the 8-bit sketch expanded on the GPU (bbmh_ext_replay, the
+    SketchRowSource analogue, learner.cpp:271-297); the last of `epochs`."""
+    out = {}
+    for name, p in (("original_libsvm", text_path), ("bbmh_8bit_k500", sketch_path)):
+        with bbmh.Replay(p, device, 32768, threads) as r:
+            secs = []
+            for _ in range(epochs):
+                t = time.perf_counter()
+                rows = nnz = 0
+                while True:
+                    n, _, _, _, rp = r.next()
+                    if n == 0:
+                        break
+                    rows += n
+                    nnz += int(rp[-1])
+                secs.append(time.perf_counter() - t)
+                r.reset()
+            out[name] = {"epoch_s": secs[-1], "epochs_s": secs, "rows": rows, "nnz": nnz,
+                         "file_bytes": os.path.getsize(p), "stats": r.stats()}
+    out["loading_time_ratio"] = out["original_libsvm"]["epoch_s"] / out["bbmh_8bit_k500"]["epoch_s"]
+    out["paper_table4_rcv1_loading_ratio"] = 29.07
+    log(f"[c4 replay] original {out['original_libsvm']['epoch_s']:.2f}s/epoch, sketch "
+        f"{out['bbmh_8bit_k500']['epoch_s']:.3f}s/epoch, ratio {out['loading_time_ratio']:.1f}")
+    return out
 
 
 def c4_reference_sample(args, path, ours_records, cb):
@@ -785,7 +816,10 @@ def c4_reference_sample(args, path, ours_records, cb):
     pre = c4_prefix(path, m, os.path.join(args.c4_dir, f"prefix_{m}.txt"))
     st, h = R.family(3, C4_DIM, K, SEED)
     t = time.perf_counter()
-    s, stats = R.sketch_file(h, pre, os.path.join(args.c4_dir, "ref.bbmh"), B, 10000, threads, False)
+    # chunk_size = ceil(n / (4 workers)) so every worker has chunks;
+    # the reference's default 10,000-doc chunk would leave one worker busy
+    chunk = max(1, -(-m // (4 * threads)))
+    s, stats = R.sketch_file(h, pre, os.path.join(args.c4_dir, "ref.bbmh"), B, chunk, threads, False)
     secs = time.perf_counter() - t
     R.destroy(h)
     if s != 0:
@@ -797,7 +831,7 @@ def c4_reference_sample(args, path, ours_records, cb):
             "text_GBps": os.path.getsize(pre) / secs / 1e9,
             "read_s": stats.read_seconds, "compute_s": stats.compute_seconds, "wall_s": secs,
             "sample": f"bbmh_sketch_file (4U-bit) on the first {m} docs of the C4 text, "
-                      f"workers={threads}; rate extrapolated to the full workload",
+                      f"workers={threads}, chunk_size={chunk}; rate extrapolated to the full workload",
             **host_info()}
 
 
@@ -814,7 +848,8 @@ def run_c4_reference(args):
     secs = []
     for i in range(args.warmup + args.steps):
         t = time.perf_counter()
-        s, _ = R.sketch_file(h, pre, os.path.join(args.c4_dir, "ref.bbmh"), B, 10000, threads, False)
+        s, _ = R.sketch_file(h, pre, os.path.join(args.c4_dir, "ref.bbmh"), B,
+                             max(1, -(-m // (4 * threads))), threads, False)
         if i >= args.warmup:
             secs.append(time.perf_counter() - t)
     R.destroy(h)

@@ -147,6 +147,40 @@ typedef struct bbmh_ext_pipeline_profile {
 } bbmh_ext_pipeline_profile;
 BBMH_API bbmh_status bbmh_ext_last_pipeline_profile(bbmh_ext_pipeline_profile* out);
 
+/* Epoch replay (the consumer of sketch files; the reference's RowSource,
+ * learner.cpp:215-312): a corpus streamed as batches of device CSR rows, once
+ * per epoch. For a BBMH sketch every record becomes the row of its k one-hot
+ * features in the 2^b*k expansion, ones[j] = j*2^b + code_j ascending, and
+ * a flagged empty record an empty row (SketchRowSource, learner.cpp:271-297;
+ * expansion.cpp:17-27). Record blocks are read ahead in page-locked memory
+ * and expanded on `device`. A LibSVM or BBCV corpus gives its rows as the
+ * sketch loader parses them (binary values). Header errors are
+ * SketchReader's (sketch.cpp:143-163); a truncated sketch returns its
+ * complete records, then fails with BBMH_E_IO "short read". */
+typedef struct bbmh_ext_replay bbmh_ext_replay;
+typedef struct bbmh_ext_replay_info {
+    int32_t sketch;        /* 1: BBMH sketch, 0: LibSVM / BBCV corpus */
+    uint32_t scheme, k, b; /* sketch header (0 for a corpus) */
+    uint64_t dim, seed, count;
+    uint64_t expanded_dim; /* 2^b * k (expanded_dim, expansion.cpp:9-15) */
+} bbmh_ext_replay_info;
+typedef struct bbmh_ext_replay_stats {
+    uint64_t epochs, rows, nnz;
+    double io_seconds, parse_seconds, expand_seconds;
+} bbmh_ext_replay_stats;
+BBMH_API bbmh_status bbmh_ext_replay_open(const char* path, int32_t device, uint64_t max_rows,
+                                          uint32_t threads, bbmh_ext_replay** out,
+                                          bbmh_ext_replay_info* info_out /* nullable */);
+/* Next batch: *rows_out rows (0 at the end of the epoch); d_row_ptr (rows+1,
+ * from 0) and d_indices on the device, labels and row_ptr_host on the host,
+ * all owned by the replay and valid until its next call. Outputs nullable. */
+BBMH_API bbmh_status bbmh_ext_replay_next(bbmh_ext_replay* replay, uint64_t* rows_out,
+                                          const uint64_t** d_row_ptr, const uint32_t** d_indices,
+                                          const int8_t** labels, const uint64_t** row_ptr_host);
+BBMH_API bbmh_status bbmh_ext_replay_reset(bbmh_ext_replay* replay);
+BBMH_API bbmh_status bbmh_ext_replay_get_stats(const bbmh_ext_replay* replay, bbmh_ext_replay_stats* out);
+BBMH_API void bbmh_ext_replay_close(bbmh_ext_replay* replay);
+
 /* Monotonic per-process counters of which routes ran: "kernel_launches",
  * "h2d_bytes", "d2h_bytes", "peer_copy_bytes", "zero_copy_calls",
  * "delta16_chunks", "raw_chunks", "range_shards", "device_id_batches". */

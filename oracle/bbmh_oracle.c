@@ -168,6 +168,19 @@ static uint32_t fam_map(const orc_family* f, uint32_t j, uint32_t t) {
 }
 
 /* HashFamily::build, hash_family.cpp:53-119 (+ capi.cpp:97-101 scheme_of) */
+/* Permutation table j of a family (hash_family.cpp:105-114): Fisher-Yates
+ * over 0..dim-1 driven by SplitMix64 seeded keyed_u64(seed, 1, j, 0). */
+void orc_perm_table(uint64_t seed, uint64_t dim, uint32_t j, uint32_t* tab) {
+    for (uint64_t t = 0; t < dim; ++t) tab[t] = (uint32_t)t;
+    splitmix rng = {orc_keyed_u64(seed, 1, j, 0)};
+    for (uint64_t t = dim - 1; t > 0; --t) {
+        uint64_t r = sm_next_below(&rng, t + 1);
+        uint32_t tmp = tab[t];
+        tab[t] = tab[r];
+        tab[r] = tmp;
+    }
+}
+
 int32_t orc_family_create(int32_t scheme, uint64_t dim, uint32_t k, uint64_t seed,
                           uint64_t prime, uint64_t perm_cap_bytes, orc_family** out) {
     t_err[0] = 0;
@@ -234,17 +247,7 @@ int32_t orc_family_create(int32_t scheme, uint64_t dim, uint32_t k, uint64_t see
             free(f);
             return set_err(ORC_E_INTERNAL, "std::bad_alloc");
         }
-        for (uint32_t j = 0; j < k; ++j) {   /* Fisher-Yates, hash_family.cpp:105-114 */
-            uint32_t* tab = f->perm + (size_t)j * dim;
-            for (uint64_t t = 0; t < dim; ++t) tab[t] = (uint32_t)t;
-            splitmix rng = {orc_keyed_u64(seed, 1, j, 0)};
-            for (uint64_t t = dim - 1; t > 0; --t) {
-                uint64_t r = sm_next_below(&rng, t + 1);
-                uint32_t tmp = tab[t];
-                tab[t] = tab[r];
-                tab[r] = tmp;
-            }
-        }
+        for (uint32_t j = 0; j < k; ++j) orc_perm_table(seed, dim, j, f->perm + (size_t)j * dim);
     }
     *out = f;
     return ORC_OK;

@@ -48,6 +48,9 @@ uint64_t orc_mod_mersenne31(uint64_t v);
 int32_t orc_family_create(int32_t scheme, uint64_t dim, uint32_t k, uint64_t seed,
                           uint64_t prime, uint64_t perm_cap_bytes, orc_family** out);
 void orc_family_destroy(orc_family* f);
+
+/* Permutation table j (dim entries) of the family with this seed. */
+void orc_perm_table(uint64_t seed, uint64_t dim, uint32_t j, uint32_t* tab);
 /* capi.cpp:142-151 -> hash_family.hpp:77-92 */
 int32_t orc_family_map(const orc_family* f, uint32_t j, uint32_t t, uint32_t* out);
 /* raw coefficients for white-box tests: 2U -> k*(a1,a2); 4U -> k*(a0..a3) */

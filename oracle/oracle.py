@@ -84,6 +84,10 @@ class CpuLib:
         self.f_last_error = getattr(L, p + "last_error")
         self.f_last_error.argtypes = []
         self.f_last_error.restype = C.c_char_p
+        self.f_perm_table = getattr(L, "orc_perm_table", None)
+        if self.f_perm_table is not None:
+            self.f_perm_table.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, u32p]
+            self.f_perm_table.restype = None
         self.f_csr = getattr(L, "orc_sketch_csr", None)
         if self.f_csr is not None:
             self.f_csr.argtypes = [C.c_void_p, u64p, u32p, C.c_uint64, C.c_uint32, u8p, u64p,
@@ -134,6 +138,13 @@ class CpuLib:
                         ptr(codes, u8p), ptr(minima, u64p), ptr(flags, u8p),
                         threads or os.cpu_count() or 1)
         return st, codes.reshape(n, cb), (minima.reshape(n, k) if want_minima else None), flags
+
+    def perm_table(self, seed, dim, j):
+        """Permutation table j of the family with this seed (port only: orc_perm_table)."""
+        assert self.f_perm_table is not None, "perm_table is a port-only helper"
+        out = np.empty(dim, np.uint32)
+        self.f_perm_table(seed, dim, j, ptr(out, u32p))
+        return out
 
     def sketch_file(self, h, inp, out, b, chunk=10000, workers=1, emit_minima=False):
         s = Stats()

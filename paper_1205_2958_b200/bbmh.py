@@ -59,6 +59,24 @@ class PipelineProfile(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ReplayInfo(C.Structure):
+    _fields_ = [("sketch", C.c_int32), ("scheme", C.c_uint32), ("k", C.c_uint32), ("b", C.c_uint32),
+                ("dim", C.c_uint64), ("seed", C.c_uint64), ("count", C.c_uint64),
+                ("expanded_dim", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class ReplayStats(C.Structure):
+    _fields_ = [("epochs", C.c_uint64), ("rows", C.c_uint64), ("nnz", C.c_uint64),
+                ("io_seconds", C.c_double), ("parse_seconds", C.c_double),
+                ("expand_seconds", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class BbmhError(RuntimeError):
     def __init__(self, status: int, message: str):
         super().__init__(f"bbmh status {status}: {message}")
@@ -115,6 +133,13 @@ def lib() -> C.CDLL:
         "bbmh_ext_get_option": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int32),
         "bbmh_ext_option_name": ([C.c_uint32], C.c_char_p),
         "bbmh_ext_counter": ([C.c_char_p, u64p], C.c_int32),
+        "bbmh_ext_replay_open": ([C.c_char_p, C.c_int32, C.c_uint64, C.c_uint32, C.POINTER(C.c_void_p),
+                                  C.POINTER(ReplayInfo)], C.c_int32),
+        "bbmh_ext_replay_next": ([C.c_void_p, u64p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                  C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)], C.c_int32),
+        "bbmh_ext_replay_reset": ([C.c_void_p], C.c_int32),
+        "bbmh_ext_replay_get_stats": ([C.c_void_p, C.POINTER(ReplayStats)], C.c_int32),
+        "bbmh_ext_replay_close": ([C.c_void_p], None),
         "bbmh_ext_last_pipeline_profile": ([C.POINTER(PipelineProfile)], C.c_int32),
         "bbmh_ext_host_budget": ([C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double), i32p],
                                  C.c_int32),
@@ -359,6 +384,88 @@ def last_pipeline_profile() -> dict:
     p = PipelineProfile()
     _check(lib().bbmh_ext_last_pipeline_profile(C.byref(p)))
     return p.as_dict()
+
+
+def device_to_numpy(ptr: int, n: int, dtype) -> np.ndarray:
+    """Copy n elements at a device address to a numpy array (through torch's
+    __cuda_array_interface__ import; for tests and tools)."""
+    import torch
+    dt = np.dtype(dtype)
+    if n == 0:
+        return np.zeros(0, dt)
+    signed = {1: "<i1", 2: "<i2", 4: "<i4", 8: "<i8"}[dt.itemsize]
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": signed, "data": (int(ptr), True),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_Cai(), device="cuda").cpu().numpy().view(dt)
+
+
+class Replay:
+    """bbmh_ext_replay_*: a corpus (BBMH sketch -> expanded one-hot rows, or
+    LibSVM / BBCV rows) streamed as device CSR batches, epoch after epoch."""
+
+    def __init__(self, path, device: int = 0, max_rows: int = 32768, threads: int = 0):
+        h = C.c_void_p()
+        info = ReplayInfo()
+        _check(lib().bbmh_ext_replay_open(None if path is None else os.fsencode(path), device,
+                                          max_rows, threads or (os.cpu_count() or 1), C.byref(h),
+                                          C.byref(info)))
+        self.handle = h
+        self.info = info.as_dict()
+
+    def next(self):
+        """-> (rows, d_row_ptr, d_indices, labels[rows] int8, row_ptr[rows+1] u64); rows = 0
+        at the end of the epoch. Device addresses are valid until the next call."""
+        n = C.c_uint64(0)
+        drp, didx, lab, hrp = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _check(lib().bbmh_ext_replay_next(self.handle, C.byref(n), C.byref(drp), C.byref(didx),
+                                          C.byref(lab), C.byref(hrp)))
+        rows = n.value
+        if rows == 0:
+            return 0, None, None, np.zeros(0, np.int8), np.zeros(1, np.uint64)
+        labels = np.ctypeslib.as_array(C.cast(lab, C.POINTER(C.c_int8)), (rows,)).copy()
+        rp = np.ctypeslib.as_array(C.cast(hrp, C.POINTER(C.c_uint64)), (rows + 1,)).copy()
+        return rows, drp.value, didx.value, labels, rp
+
+    def epoch_host(self):
+        """One epoch copied to the host: (labels, row_ptr, indices)."""
+        labs, rps, idxs, base = [], [np.zeros(1, np.uint64)], [], 0
+        while True:
+            n, drp, didx, lab, rp = self.next()
+            if n == 0:
+                break
+            labs.append(lab)
+            idxs.append(device_to_numpy(didx, int(rp[-1]), np.uint32))
+            rps.append(rp[1:] + base)
+            base += int(rp[-1])
+        return (np.concatenate(labs) if labs else np.zeros(0, np.int8), np.concatenate(rps),
+                np.concatenate(idxs) if idxs else np.zeros(0, np.uint32))
+
+    def reset(self):
+        _check(lib().bbmh_ext_replay_reset(self.handle))
+
+    def stats(self) -> dict:
+        s = ReplayStats()
+        _check(lib().bbmh_ext_replay_get_stats(self.handle, C.byref(s)))
+        return s.as_dict()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().bbmh_ext_replay_close(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def counter(name: str) -> int:

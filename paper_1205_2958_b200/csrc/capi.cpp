@@ -16,12 +16,17 @@
 #include "engine.hpp"
 #include "estimate.hpp"
 #include "options.hpp"
+#include "replay.hpp"
 #include "pipeline.hpp"
 
 using namespace bbmh;
 
 struct bbmh_family {
     std::unique_ptr<Family> impl;
+};
+
+struct bbmh_ext_replay {
+    std::unique_ptr<Replay> impl;
 };
 
 namespace {
@@ -322,6 +327,53 @@ bbmh_status bbmh_ext_get_option(const char* name, int64_t* value_out) {
 }
 
 const char* bbmh_ext_option_name(uint32_t i) { return opt_name(int(i)); }
+
+bbmh_status bbmh_ext_replay_open(const char* path, int32_t device, uint64_t max_rows, uint32_t threads,
+                                 bbmh_ext_replay** out, bbmh_ext_replay_info* info_out) {
+    return guarded([&] {
+        if (!out) fail(Errc::InvalidArgument, "out must not be NULL");
+        *out = nullptr;
+        const std::string p = require(path, "path");
+        int count = 0;
+        BBMH_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count)
+            fail(Errc::InvalidArgument, "device " + std::to_string(device) + " does not exist");
+        auto r = std::make_unique<bbmh_ext_replay>();
+        r->impl = std::make_unique<Replay>(p, device, max_rows ? max_rows : 32768, threads ? threads : 1);
+        if (info_out) {
+            const ReplayInfo& i = r->impl->info();
+            *info_out = {i.sketch ? 1 : 0, i.scheme, i.k, i.b, i.dim, i.seed, i.count, i.expanded_dim};
+        }
+        *out = r.release();
+    });
+}
+
+bbmh_status bbmh_ext_replay_next(bbmh_ext_replay* replay, uint64_t* rows_out, const uint64_t** d_row_ptr,
+                                 const uint32_t** d_indices, const int8_t** labels,
+                                 const uint64_t** row_ptr_host) {
+    return guarded([&] {
+        if (!replay) fail(Errc::InvalidArgument, "replay must not be NULL");
+        const uint64_t n = replay->impl->next(d_row_ptr, d_indices, labels, row_ptr_host);
+        if (rows_out) *rows_out = n;
+    });
+}
+
+bbmh_status bbmh_ext_replay_reset(bbmh_ext_replay* replay) {
+    return guarded([&] {
+        if (!replay) fail(Errc::InvalidArgument, "replay must not be NULL");
+        replay->impl->reset();
+    });
+}
+
+bbmh_status bbmh_ext_replay_get_stats(const bbmh_ext_replay* replay, bbmh_ext_replay_stats* out) {
+    return guarded([&] {
+        if (!replay || !out) fail(Errc::InvalidArgument, "replay and out must not be NULL");
+        const ReplayStats s = replay->impl->stats();
+        *out = {s.epochs, s.rows, s.nnz, s.io_seconds, s.parse_seconds, s.expand_seconds};
+    });
+}
+
+void bbmh_ext_replay_close(bbmh_ext_replay* replay) { delete replay; }
 
 bbmh_status bbmh_ext_last_pipeline_profile(bbmh_ext_pipeline_profile* out) {
     return guarded([&] {

@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
                                                      uint8_t* __restrict__ codes,
                                                      uint64_t* __restrict__ minima,
                                                      uint8_t* __restrict__ flags, int* err,
+                                                     unsigned long long* work,
                                                      unsigned long long* cta_trace = nullptr) {
     extern __shared__ __align__(128) uint32_t smem[];
     const uint32_t kBuf = tile + 8;
@@ -258,7 +259,20 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
     const uint32_t jcnt = min(jtile, k - j0);
 
     // ---- producer state (thread 0 only) ----
+    // Documents after the first wave are handed out dynamically: `work` is a
+    // ticket counter (work[0]) and an exit counter (work[1]), both zero at
+    // launch; the last CTA to exit zeroes them for the launch that reuses the
+    // slot. With static round-robin assignment the CTAs sharing an SM drifted
+    // apart under the warp scheduler's priorities -- the first finished after
+    // a fifth of the kernel and the SM ran at 60% of its resident CTAs on
+    // average (tools/residency_probe.cu, profiles/round2). The next ticket is
+    // fetched one document ahead, so the atomic's latency is hidden. Without
+    // `work` (several j-tiles per document) the assignment stays static.
     uint64_t p_doc = blockIdx.x, p_off = 0, p_beg = 0, p_end = 0;
+    uint64_t p_next = 0;
+    auto fetch_next = [&]() -> uint64_t {
+        return work ? gridDim.x + atomicAdd(&work[0], 1ull) : p_doc + gridDim.x;
+    };
     auto load_bounds = [&]() {
         if (p_doc < n_docs) {
             p_beg = row_ptr[p_doc];
@@ -296,7 +310,8 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         }
         desc[bi] = it;
         if (it.last) {
-            p_doc += gridDim.x;
+            p_doc = p_next;
+            if (p_doc < n_docs) p_next = fetch_next();
             p_off = 0;
             load_bounds();
         } else {
@@ -308,6 +323,7 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        p_next = fetch_next();
         load_bounds();
         issue(0);
     }
@@ -414,6 +430,14 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
             }
         }
         __syncthreads();  // buffer bi and s_code free; desc[bi ^ 1] visible
+    }
+    if (work && tid == 0) {
+        // every ticket this CTA will take has been taken; the last CTA out resets
+        __threadfence();
+        if (atomicAdd(&work[1], 1ull) == (unsigned long long)gridDim.x - 1) {
+            work[0] = 0;
+            work[1] = 0;
+        }
     }
     if constexpr (TRACE) {
         if (tid == 0) {
@@ -555,6 +579,33 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
     }
 }
 
+// Ticket counters of the persistent sketch kernel (see sketch_kernel): a pool
+// of zeroed {ticket, exit} pairs per device, taken round-robin per launch;
+// each launch leaves its pair zeroed, and a pair is reused only 1,023
+// launches later.
+unsigned long long* work_slot(int dev) {
+    constexpr int kSlots = 1024;
+    static std::mutex mu;
+    static std::map<int, unsigned long long*> pools;
+    static std::atomic<uint64_t> seq{0};
+    unsigned long long* pool = nullptr;
+    {
+        std::lock_guard lk(mu);
+        auto it = pools.find(dev);
+        if (it == pools.end()) {
+            if (cudaMalloc(&pool, kSlots * 2 * sizeof(unsigned long long)) != cudaSuccess ||
+                cudaMemset(pool, 0, kSlots * 2 * sizeof(unsigned long long)) != cudaSuccess) {
+                cudaGetLastError();
+                if (pool) cudaFree(pool);
+                return nullptr;  // static assignment
+            }
+            it = pools.emplace(dev, pool).first;
+        }
+        pool = it->second;
+    }
+    return pool + 2 * (seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+}
+
 template <int SCHEME, bool POW2, int J, bool TRACE = false>
 void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* row_ptr,
                 uint64_t base, const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
@@ -621,8 +672,9 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     if (gx > n) gx = n;
     dim3 grid((unsigned)gx, sh.jtiles);
     const cudaError_t pre = cudaPeekAtLastError();
+    unsigned long long* work = sh.jtiles == 1 && opt(Opt::DynamicDocs) ? work_slot(dev) : nullptr;
     kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr, base, idx, n, b, sh.jtile, (uint32_t)tile, codes,
-                                     minima, flags, err, cta_trace);
+                                     minima, flags, err, work, cta_trace);
     if (const cudaError_t e = cudaPeekAtLastError(); e != cudaSuccess)
         fprintf(stderr, "bbmh: sketch launch failed (%s; before launch: %s) grid %u x %u tpb %d smem %zu\n",
                 cudaGetErrorString(e), cudaGetErrorString(pre), grid.x, grid.y, sh.tpb, smem);

@@ -25,6 +25,7 @@ constexpr Def kDefs[] = {
     {"shape_j", 0},
     {"shape_tpb", 0},
     {"carveout", -1},
+    {"dynamic_docs", 1},
     {"split_small_k", 1},
     {"perm_tablewise", -1},
     {"perm_scratch_mb", 2048},

@@ -168,3 +168,16 @@ def test_port_files_match_reference_random(port, ref, tmp_path):
                 assert outs[0] == outs[3] and outs[1] == outs[4] and outs[2] == outs[5]
         port.destroy(hp)
         ref.destroy(hr)
+
+
+def test_oracle_perm_table_equals_reference_maps(port, ref):
+    """orc_perm_table (one Fisher-Yates table, the checker of the GPU-built
+    tables at full size) against the reference's own map() (hash_family.cpp:105-114)."""
+    dim, k, seed = 5003, 9, 1234
+    st, h = ref.family(0, dim, k, seed, 0, 1 << 30)
+    assert st == 0
+    for j in (0, 4, k - 1):
+        tab = port.perm_table(seed, dim, j)
+        want = np.array([ref.map(h, j, t)[1] for t in range(dim)], np.uint32)
+        assert np.array_equal(tab, want), j
+    ref.destroy(h)

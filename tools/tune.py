@@ -44,6 +44,7 @@ def main():
             bbmh.set_option("ctas_per_sm", g.get("CTAS", 0))
             bbmh.set_option("smem_cap", g.get("SMEM_CAP", 1))
             bbmh.set_option("carveout", g.get("CARVEOUT", -1))
+            bbmh.set_option("dynamic_docs", g.get("DYN", 1))
 
             def step():
                 fam.sketch_csr_device(d_rp.data_ptr(), d_idx.data_ptr(), n, bench.B,
