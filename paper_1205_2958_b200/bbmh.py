@@ -396,7 +396,7 @@ def device_to_numpy(ptr: int, n: int, dtype) -> np.ndarray:
     signed = {1: "<i1", 2: "<i2", 4: "<i4", 8: "<i8"}[dt.itemsize]
 
     class _Cai:
-        __cuda_array_interface__ = {"shape": (int(n),), "typestr": signed, "data": (int(ptr), True),
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": signed, "data": (int(ptr), False),
                                     "version": 3, "strides": None}
     return torch.as_tensor(_Cai(), device="cuda").cpu().numpy().view(dt)
 

@@ -497,7 +497,10 @@ private:
                     any |= b.n > n0;
                     continue;
                 }
-                if (g == 0 || g == 2) break;  // end of input / batch full
+                if (g == 0 || g == 2) {  // end of input / batch full (this block may have added rows)
+                    any |= b.n > n0;
+                    break;
+                }
                 // g < 0: the block is parsed by the CPU path below
             }
             // gather complete lines (as NUL-terminated spans) for this round

@@ -241,7 +241,6 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
                                                      uint8_t* __restrict__ codes,
                                                      uint64_t* __restrict__ minima,
                                                      uint8_t* __restrict__ flags, int* err,
-                                                     unsigned long long* work,
                                                      unsigned long long* cta_trace = nullptr) {
     extern __shared__ __align__(128) uint32_t smem[];
     const uint32_t kBuf = tile + 8;
@@ -259,20 +258,16 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
     const uint32_t jcnt = min(jtile, k - j0);
 
     // ---- producer state (thread 0 only) ----
-    // Documents after the first wave are handed out dynamically: `work` is a
-    // ticket counter (work[0]) and an exit counter (work[1]), both zero at
-    // launch; the last CTA to exit zeroes them for the launch that reuses the
-    // slot. With static round-robin assignment the CTAs sharing an SM drifted
-    // apart under the warp scheduler's priorities -- the first finished after
-    // a fifth of the kernel and the SM ran at 60% of its resident CTAs on
-    // average (tools/residency_probe.cu, profiles/round2). The next ticket is
-    // fetched one document ahead, so the atomic's latency is hidden. Without
-    // `work` (several j-tiles per document) the assignment stays static.
+    // Documents go round-robin: CTA x takes x, x + gridDim.x, ... Under the
+    // warp scheduler's priorities the CTAs sharing an SM drift apart (the
+    // first finishes after a fifth of the kernel, tools/residency_probe.cu),
+    // but the SM's pipes stay as busy with fewer resident CTAs: handing out
+    // documents from an atomic ticket counter kept every CTA resident to the
+    // end and gained 1.8%, yet its code cost the item loop its uniform control
+    // flow (ptxas moved the loop bounds and LDS addresses from uniform to
+    // vector registers: +4 IMAD per iteration), a net loss of 3%
+    // (profiles/round2/dynamic_tickets_ab.jsonl).
     uint64_t p_doc = blockIdx.x, p_off = 0, p_beg = 0, p_end = 0;
-    uint64_t p_next = 0;
-    auto fetch_next = [&]() -> uint64_t {
-        return work ? gridDim.x + atomicAdd(&work[0], 1ull) : p_doc + gridDim.x;
-    };
     auto load_bounds = [&]() {
         if (p_doc < n_docs) {
             p_beg = row_ptr[p_doc];
@@ -310,8 +305,7 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         }
         desc[bi] = it;
         if (it.last) {
-            p_doc = p_next;
-            if (p_doc < n_docs) p_next = fetch_next();
+            p_doc += gridDim.x;
             p_off = 0;
             load_bounds();
         } else {
@@ -323,7 +317,6 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        p_next = fetch_next();
         load_bounds();
         issue(0);
     }
@@ -431,14 +424,6 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
         }
         __syncthreads();  // buffer bi and s_code free; desc[bi ^ 1] visible
     }
-    if (work && tid == 0) {
-        // every ticket this CTA will take has been taken; the last CTA out resets
-        __threadfence();
-        if (atomicAdd(&work[1], 1ull) == (unsigned long long)gridDim.x - 1) {
-            work[0] = 0;
-            work[1] = 0;
-        }
-    }
     if constexpr (TRACE) {
         if (tid == 0) {
             unsigned long long t1;
@@ -471,7 +456,8 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
                                                            uint64_t n_docs, uint32_t b,
                                                            uint8_t* __restrict__ codes,
                                                            uint64_t* __restrict__ minima,
-                                                           uint8_t* __restrict__ flags, int* err) {
+                                                           uint8_t* __restrict__ flags, int* err,
+                                                           unsigned long long* work) {
     __shared__ uint32_t s_code[4][J];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
     const uint32_t k = Fm.k;
@@ -507,9 +493,18 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
         for (int i = 0; i < kQ; ++i)
             nx[i] = lane + 32 * i < nq ? __ldg(q4 + lane + 32 * i) : make_uint4(0, 0, 0, 0);
     };
+    // documents after the first wave come from a ticket counter, one ticket
+    // ahead; round-robin without `work`
+    auto fetch_next = [&](uint64_t cur) -> uint64_t {
+        if (!work) return cur + stride;
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(&work[0], 1ull);
+        return stride + __shfl_sync(0xffffffffu, t, 0);
+    };
     uint64_t doc = (uint64_t)blockIdx.x * W + warp;
+    uint64_t nxt = doc < n_docs ? fetch_next(doc) : n_docs;
     if (doc < n_docs) describe(doc);
-    for (; doc < n_docs; doc += stride) {
+    for (; doc < n_docs; doc = nxt, nxt = doc < n_docs ? fetch_next(doc) : n_docs) {
         uint32_t m[J];
 #pragma unroll
         for (int r = 0; r < J; ++r) m[r] = 0xffffffffu;
@@ -539,7 +534,7 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
         const uint64_t t0 = head + 4 * nq;
         if (t0 + lane < nnz) eval(__ldg(ids + t0 + lane));
         const bool empty = nnz == 0;
-        if (doc + stride < n_docs) describe(doc + stride);  // loads in flight during the merge
+        if (nxt < n_docs) describe(nxt);  // loads in flight during the merge
         // merge the 32 lanes' minima, function by function
 #pragma unroll
         for (int r = 0; r < J; ++r) {
@@ -577,9 +572,16 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
         }
         __syncwarp();
     }
+    if (work && lane == 0) {  // the last warp out resets the counters
+        __threadfence();
+        if (atomicAdd(&work[1], 1ull) == stride - 1) {
+            work[0] = 0;
+            work[1] = 0;
+        }
+    }
 }
 
-// Ticket counters of the persistent sketch kernel (see sketch_kernel): a pool
+// Ticket counters of the small-k kernel (see sketch_split_kernel): a pool
 // of zeroed {ticket, exit} pairs per device, taken round-robin per launch;
 // each launch leaves its pair zeroed, and a pair is reused only 1,023
 // launches later.
@@ -672,9 +674,8 @@ void launch_one(const KernelFamily& F, const LaunchShape& sh, const uint64_t* ro
     if (gx > n) gx = n;
     dim3 grid((unsigned)gx, sh.jtiles);
     const cudaError_t pre = cudaPeekAtLastError();
-    unsigned long long* work = sh.jtiles == 1 && opt(Opt::DynamicDocs) ? work_slot(dev) : nullptr;
     kern<<<grid, sh.tpb, smem, st>>>(F, row_ptr, base, idx, n, b, sh.jtile, (uint32_t)tile, codes,
-                                     minima, flags, err, work, cta_trace);
+                                     minima, flags, err, cta_trace);
     if (const cudaError_t e = cudaPeekAtLastError(); e != cudaSuccess)
         fprintf(stderr, "bbmh: sketch launch failed (%s; before launch: %s) grid %u x %u tpb %d smem %zu\n",
                 cudaGetErrorString(e), cudaGetErrorString(pre), grid.x, grid.y, sh.tpb, smem);
@@ -723,8 +724,11 @@ void launch_split(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
     uint64_t grid = (uint64_t)device_sms() * occ;
     const uint64_t need = (n + 3) / 4;
     if (grid > need) grid = need;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    unsigned long long* work = opt(Opt::DynamicDocs) ? work_slot(dev) : nullptr;
     sketch_split_kernel<SCHEME, POW2, FF><<<(unsigned)grid, kTpb, 0, st>>>(
-        F, row_ptr, base, idx, n, b, codes, minima, flags, err);
+        F, row_ptr, base, idx, n, b, codes, minima, flags, err, work);
     g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

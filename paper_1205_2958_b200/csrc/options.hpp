@@ -19,7 +19,7 @@ enum class Opt : int {
     ShapeJ,         // force J functions per thread (0: choose_shape)
     ShapeTpb,       // force threads per CTA (0: choose_shape)
     Carveout,       // shared-memory carveout % for the sketch kernels (-1: driver default)
-    DynamicDocs,    // persistent sketch kernel takes documents from a ticket counter (1) or round-robin (0)
+    DynamicDocs,    // small-k sketch kernel takes documents from a ticket counter (1) or round-robin (0)
     SplitSmallK,    // small-k lane-split kernel (1) or the persistent kernel (0)
     PermTablewise,  // permutation schedule: -1 auto, 0 document-outer, 1 table-outer
     PermScratchMb,  // table-outer schedule: device scratch budget per pass group (MiB)

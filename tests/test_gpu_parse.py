@@ -125,3 +125,24 @@ def test_gpu_parse_lines_longer_than_the_window(bb, ref, tmp_path):
         (g, launches) = _sketch(bb, str(path), str(tmp_path / "gpu.bbmh"), gpu=True, block=block)
         assert g == cpu, block
         assert launches > 4
+
+
+def test_gpu_parse_first_block_over_the_batch_row_budget(bb, ref, tmp_path):
+    """More rows in the first device block than a loader batch takes (short
+    rows: 60,000 in ~5 MB against 32,768-row batches): the block's prefix fills
+    the batch and the rest starts the next one -- no row is lost."""
+    rng = np.random.default_rng(21)
+    lines = []
+    for i in range(60_000):
+        ids = np.unique(rng.integers(0, 1 << 22, int(rng.integers(0, 12)))) + 1
+        lines.append(("+1" if i % 2 else "-1") + "".join(" %d:1" % t for t in ids))
+    path = tmp_path / "short.txt"
+    path.write_text("\n".join(lines) + "\n")
+    st, h = ref.family(1, 1 << 22, 64, 42)
+    s, _ = ref.sketch_file(h, str(path), str(tmp_path / "ref.bbmh"), 8, 10000, 4, False)
+    ref.destroy(h)
+    assert s == 0
+    want = (tmp_path / "ref.bbmh").read_bytes()
+    for block in (None, 1 << 20):
+        (g, _) = _sketch(bb, str(path), str(tmp_path / "gpu.bbmh"), gpu=True, block=block)
+        assert g[0] == 0 and g[1] == want, block
