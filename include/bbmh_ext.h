@@ -31,12 +31,14 @@ BBMH_API bbmh_status bbmh_ext_sketch_csr(const bbmh_family* family, const uint64
  * cudaStream_t, NULL = legacy default stream) and returns without
  * synchronising. row_ptr values are offsets into d_indices after subtracting
  * `index_base` (lets a caller pass a slice of a larger row_ptr).
- * Ids are fetched with bulk copies in whole 16-byte granules, so the granule
- * holding the last id (d_indices + row_ptr[n] - index_base) is read to its
- * end: up to 12 bytes past the last id, never across a page. An allocation
- * whose size is a multiple of 16 bytes (or with 12 bytes of slack) keeps
- * compute-sanitizer memcheck quiet. The host entry points handle this
- * themselves. */
+ * Ids are fetched with bulk copies in whole 16-byte granules: the granule
+ * holding a row's first id is read from its start and the granule holding its
+ * last id to its end -- up to 12 bytes before d_indices + row_ptr[0] -
+ * index_base and up to 12 bytes past the last id, never across a page; the
+ * values there are never used. An allocation that starts 16-byte aligned
+ * (cudaMalloc's always do) and whose size is a multiple of 16 bytes (or has
+ * 12 bytes of slack) keeps compute-sanitizer memcheck quiet. The host entry
+ * points handle this themselves. */
 BBMH_API bbmh_status bbmh_ext_sketch_csr_device(const bbmh_family* family,
                                                 const uint64_t* d_row_ptr, uint64_t index_base,
                                                 const uint32_t* d_indices, uint64_t n,

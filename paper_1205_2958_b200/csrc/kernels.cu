@@ -726,7 +726,13 @@ void launch_split(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
     if (grid > need) grid = need;
     int dev = 0;
     cudaGetDevice(&dev);
-    unsigned long long* work = opt(Opt::DynamicDocs) ? work_slot(dev) : nullptr;
+    // Tickets: +7-17% for 2U at k = 8..32 and 4U at k = 1..16 (the warps
+    // sharing an SM drift apart under round-robin assignment), but at 2U
+    // k <= 2 a document is so short that the single counter serialises the
+    // warps (k = 1: 1.73 -> 1.11 T evals/s): those stay round-robin
+    // (profiles/round2/dynamic_tickets_smallk_ab.jsonl).
+    const bool tickets = opt(Opt::DynamicDocs) && !(SCHEME == S_2U && FF <= 2);
+    unsigned long long* work = tickets ? work_slot(dev) : nullptr;
     sketch_split_kernel<SCHEME, POW2, FF><<<(unsigned)grid, kTpb, 0, st>>>(
         F, row_ptr, base, idx, n, b, codes, minima, flags, err, work);
     g_launches.fetch_add(1, std::memory_order_relaxed);

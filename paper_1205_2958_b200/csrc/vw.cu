@@ -184,18 +184,9 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         Buf<int> d_vals, d_vals2, d_sums, d_osums, d_nrun, d_nsel, d_err;
         Buf<unsigned char> d_flags, d_tmp;
     };
-    static std::mutex dev_mu;
-    static std::vector<std::unique_ptr<DevBufs>> dev_bufs;
-    std::lock_guard dev_lk(dev_mu);
-    {
-        int cur = 0;
-        BBMH_CUDA(cudaGetDevice(&cur));
-        if (size_t(cur) >= dev_bufs.size()) dev_bufs.resize(cur + 1);
-        if (!dev_bufs[cur]) dev_bufs[cur] = std::make_unique<DevBufs>();
-    }
-    int cur_dev = 0;
-    BBMH_CUDA(cudaGetDevice(&cur_dev));
-    DevBufs& D = *dev_bufs[cur_dev];
+    // buffers live for the call (the library keeps no device or page-locked
+    // memory between VW calls)
+    DevBufs D;
     auto& d_rp = D.d_rp;
     auto& d_ids = D.d_ids;
     auto& d_keys = D.d_keys;
@@ -230,14 +221,8 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         d_flags.reserve(cap);
         d_rp.reserve((1u << 16) + 1);
     }
-    // page-locked result buffers are kept across calls (pinning ~200 MB costs
-    // far more than a batch); calls are serialised on them
-    static std::mutex host_mu;
-    static HostBuf<unsigned long long> keys;
-    static HostBuf<int> sums;
-    std::lock_guard host_lk(host_mu);
-    keys.reserve((1u << 24) + (1u << 22));
-    sums.reserve((1u << 24) + (1u << 22));
+    HostBuf<unsigned long long> keys;
+    HostBuf<int> sums;
     Batch batch;
     uint64_t rows_written = 0;
     int dev = 0, sms = 148;
@@ -251,6 +236,7 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         if (!reader->fill(batch, 1u << 16, 1u << 24)) break;
         trace("vw: filled");
         const uint64_t n = batch.n, nid = batch.nids();
+        uint64_t n_ok = n;  // rows to write (those before a failing one)
         int nsel = 0;
         if (nid) {
             d_rp.reserve(n + 1);
@@ -304,8 +290,18 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
             BBMH_CUDA(cudaMemcpyAsync(&nsel, d_nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
             BBMH_CUDA(cudaMemcpyAsync(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
             BBMH_CUDA(cudaStreamSynchronize(st));
-            if (err)
-                fail(Errc::UnsupportedUniverse, "feature id must be < 2^31-1 for the sign hash");
+            if (err) {
+                // the reference writes every row before the first offending
+                // one, then fails (vw.cpp:61-77): keep only those rows
+                uint64_t bad_row = 0;
+                for (uint64_t i = 0; i < nid; ++i)
+                    if (batch.ids[i] >= 0x7fffffffu) {
+                        bad_row = uint64_t(std::upper_bound(batch.row_ptr.begin(), batch.row_ptr.end(), i) -
+                                           batch.row_ptr.begin()) - 1;
+                        break;
+                    }
+                n_ok = bad_row;
+            }
             keys.reserve(size_t(nsel) + 1);
             sums.reserve(size_t(nsel) + 1);
             if (nsel) {
@@ -318,12 +314,12 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         // write_libsvm (dataio.cpp:115-125): "%+d" then " %u:%g" per entry.
         // Rows are formatted in parallel ranges (the text is ~12 bytes per
         // entry: this was the single-threaded bottleneck) and written in order.
-        const unsigned T = n < 512 ? 1u : std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        const unsigned T = n_ok < 512 ? 1u : std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         // entry <= 22 chars (" 4294967296:-999999"), row head <= 3 + newline
         std::vector<std::vector<char>> parts(T);
         std::vector<size_t> used(T, 0);
         auto fmt = [&](unsigned w) {
-            const uint64_t r0 = n * w / T, r1 = n * (w + 1) / T;
+            const uint64_t r0 = n_ok * w / T, r1 = n_ok * (w + 1) / T;
             // first entry of row r0: keys are sorted by (row << 32 | bin)
             uint64_t e = std::lower_bound(keys.p, keys.p + nsel, (unsigned long long)r0 << 32) - keys.p;
             uint64_t e_end = std::lower_bound(keys.p, keys.p + nsel, (unsigned long long)r1 << 32) - keys.p;
@@ -362,7 +358,8 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         trace("vw: formatted");
         for (unsigned w = 0; w < T; ++w) write_all(out, parts[w].data(), used[w]);
         trace("vw: written");
-        rows_written += n;
+        rows_written += n_ok;
+        if (n_ok < n) fail(Errc::UnsupportedUniverse, "feature id must be < 2^31-1 for the sign hash");
     }
     return rows_written;
 }

@@ -50,3 +50,19 @@ def test_vw_errors_match_reference(bb, ref, tmp_path):
         r = _vw(ref.lib, ref.last_error, c, o, bins, 1)
         g = _vw(bb.lib(), bb.last_error, c, o, bins, 1)
         assert g[0] == r[0] and g[1].replace(str(tmp_path), "") == r[1].replace(str(tmp_path), ""), (corpus, out, bins, g, r)
+
+
+def test_vw_writes_the_rows_before_a_bad_id(bb, ref, tmp_path):
+    """An id >= 2^31-1 in row r fails the call after rows 0..r-1 are written,
+    as the reference's row-by-row loop leaves them (vw.cpp:61-77); those rows
+    equal the reference's output for the corpus cut before row r."""
+    rng = np.random.default_rng(4)
+    rows = [(1 if i % 2 else -1, np.unique(rng.integers(0, 1 << 30, 50)).astype(np.uint32)) for i in range(300)]
+    bad = rows[:123] + [(1, np.array([5, (1 << 31) - 1], np.uint32))] + rows[123:]
+    (tmp_path / "bad.bbcv").write_bytes(bbcv_bytes(1 << 31, bad))
+    (tmp_path / "head.bbcv").write_bytes(bbcv_bytes(1 << 31, rows[:123]))
+    g = _vw(bb.lib(), bb.last_error, str(tmp_path / "bad.bbcv"), str(tmp_path / "g.txt"), 1 << 12, 3)
+    assert g[0] == bb.E_UNSUPPORTED_UNIVERSE and "2^31-1" in g[1]
+    r = _vw(ref.lib, ref.last_error, str(tmp_path / "head.bbcv"), str(tmp_path / "r.txt"), 1 << 12, 3)
+    assert r[0] == 0
+    assert (tmp_path / "g.txt").read_bytes() == (tmp_path / "r.txt").read_bytes()
