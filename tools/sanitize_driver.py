@@ -4,7 +4,8 @@ power-of-two and general D, 4U-mod, permutation in both schedules, k
 spanning several CTAs, rows longer than one shared-memory tile, empty rows),
 the file pipeline on BBCV and on LibSVM text (GPU parser + CPU fallback),
 the 2-byte id transfer, expansion to BBCV and LibSVM text, fused scoring,
-predict on a BBMH file, all-pairs match counts and the VW projection.
+predict on a BBMH file, all-pairs match counts, the VW projection, the small-k
+kernel with document tickets, range-sharded LibSVM loading and epoch replay.
 No torch; ctypes only. Usage: compute-sanitizer --tool memcheck python
 tools/sanitize_driver.py"""
 import ctypes as C
@@ -79,6 +80,30 @@ def main():
         lib.bbmh_vw_project_file.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64]
         assert lib.bbmh_vw_project_file(corpus.encode(), os.path.join(td, "v.txt").encode(),
                                         1 << 10, 3) == 0, bbmh.last_error()
+    # small-k lane-split kernel with document tickets (2U k = 8, 4U k = 4)
+    for scheme, k_small in ((1, 8), (3, 4)):
+        with bbmh.Family(scheme, 1 << 20, k_small, 42) as f:
+            f.sketch_csr(rp, idx, 8, want_minima=True)
+    with tempfile.TemporaryDirectory() as td:
+        rows = [(1 if i % 2 else -1, idx[int(rp[i]):int(rp[i + 1])]) for i in range(12)]
+        txt = os.path.join(td, "c.txt")
+        lines = ["%+d" % lab + "".join(" %d:1" % (t + 1) for t in ids) for lab, ids in rows]
+        open(txt, "w").write("\n".join(lines * 20) + "\n")
+        # range-sharded LibSVM loading: two lanes on this device, three ranges each
+        bbmh.set_devices([0, 0])
+        bbmh.set_option("range_shards", 3)
+        sk = os.path.join(td, "r.bbmh")
+        with bbmh.Family(1, 1 << 20, 30, 42) as f:
+            f.sketch_file(txt, sk, 4, 5, 2)
+        bbmh.set_devices([0])
+        bbmh.set_option("range_shards", 1)
+        # epoch replay of the sketch (expansion kernel) and of the text (loader)
+        for path in (sk, txt):
+            with bbmh.Replay(path, 0, 7) as r:
+                for _ in range(2):
+                    while r.next()[0]:
+                        pass
+                    r.reset()
     k, b = 100, 4
     cb = (k * b + 7) // 8
     A = rng.integers(0, 256, (37, cb), dtype=np.uint8)
