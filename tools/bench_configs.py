@@ -130,7 +130,7 @@ def run_c3(n_docs):
           "roofline": {"bound": "l2_random_gather", "achieved": gps, "peak": l2,
                        "frac": gps / l2, "unit": "gathers/s",
                        "peak_how": "intpeak.l2_gathers: 64 MB table, 8 CTAs x 256 threads per SM"},
-          "sector_bound_gathers_per_s_at_hbm": 6461.2e9 / 32})
+          "sector_bound_gathers_per_s_at_hbm": bench.hbm_peak()[0] * 1e9 / 32})
     f.close()
     del d_rp, d_idx, d_codes
     torch.cuda.empty_cache()
@@ -143,7 +143,6 @@ def run_ksweep(n_docs):
     algorithmic bytes (ids in, codes + flags out) per launch."""
     dev = torch.device("cuda", 0)
     d_rp, d_idx = bench.make_corpus_device(torch, n_docs, bench.NNZ, bench.D_WEBSPAM, 5, dev)
-    peaks = bench.int_peaks()
     b = 8
     for scheme, sid, dim in (("2u", 1, 1 << 24), ("4u-bit", 3, bench.D_WEBSPAM)):
         for k in (1, 8, 32, 200, 500):
@@ -157,11 +156,13 @@ def run_ksweep(n_docs):
                                                       stream=st.cuda_stream), reps=3)
             evals = n_docs * bench.NNZ * k
             bytes_ = n_docs * bench.NNZ * 4 + (n_docs + 1) * 8 + n_docs * (cb + 1)
-            rf = bench.roofline_int(scheme, dim, evals / ms * 1e3, 1965.0, peaks)
-            hbm_frac = bytes_ / (ms * 1e-3) / 6461.2e9
+            # the SURVEY §8d contract at 1,965 MHz (the clock these runs hold)
+            rf = bench.roofline_contract(scheme, evals / ms * 1e3, 1965.0)
+            hbm_gbs_peak = bench.hbm_peak()[0]
+            hbm_frac = bytes_ / (ms * 1e-3) / (hbm_gbs_peak * 1e9)
             # time each roofline alone would allow; the larger one binds
             t_int = evals / (rf["peak"] * 1e9) if rf else None
-            t_hbm = bytes_ / 6461.2e9
+            t_hbm = bytes_ / (hbm_gbs_peak * 1e9)
             emit({"config": "ksweep", "scheme": scheme, "k": k, "docs": n_docs, "kernel_ms": ms,
                   "hash_evals_per_s": evals / ms * 1e3, "docs_per_s": n_docs / ms * 1e3,
                   "int_frac": rf["frac"] if rf else None, "hbm_gbs": bytes_ / ms / 1e6,
