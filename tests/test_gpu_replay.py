@@ -120,3 +120,26 @@ def test_replay_original_libsvm_rows(bb, tmp_path):
             assert np.array_equal(grp, np.array(rp, np.uint64))
             assert np.array_equal(gidx, np.array(idx, np.uint32))
             r.reset()
+
+
+def test_replay_original_bbcv_rows(bb, tmp_path):
+    """A BBCV corpus through the replay API (BinaryRowSource, learner.cpp:215-235):
+    its rows, labels included, in order, every epoch."""
+    from helpers import bbcv_bytes
+    rng = np.random.default_rng(19)
+    rows = []
+    for i in range(900):
+        n = int(rng.integers(0, 400)) if i % 17 else 0
+        rows.append((1 if i % 3 else -1, np.unique(rng.integers(0, 1 << 24, n)).astype(np.uint32)))
+    src = tmp_path / "c.bbcv"
+    src.write_bytes(bbcv_bytes(1 << 24, rows))
+    want_rp = np.zeros(len(rows) + 1, np.uint64)
+    want_rp[1:] = np.cumsum([r[1].size for r in rows])
+    with bb.Replay(str(src), 0, 250) as r:
+        assert r.info["sketch"] == 0
+        for _ in range(2):
+            lab, grp, gidx = r.epoch_host()
+            assert np.array_equal(lab, np.array([r_[0] for r_ in rows], np.int8))
+            assert np.array_equal(grp, want_rp)
+            assert np.array_equal(gidx, np.concatenate([r_[1] for r_ in rows]))
+            r.reset()
