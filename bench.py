@@ -690,7 +690,9 @@ def run_c4(args, torch, dev, rank, world, local, barrier, max_over_ranks, bbmh):
     torch.cuda.empty_cache()
     launches_kernel = bbmh.kernel_launches() - launches0
 
-    # ---- e2e: bbmh_sketch_file on LibSVM text of the C4 shape (rank 0's host) ----
+    # ---- e2e: bbmh_sketch_file on LibSVM text of the C4 shape (each rank its own file) ----
+    if world > 1:
+        args.c4_dir = os.path.join(args.c4_dir, f"rank{rank}")
     path, text_bytes, text_docs = c4_corpus(args)
     threads = os.cpu_count() or 1
     e2e = {}

@@ -33,6 +33,7 @@ constexpr Def kDefs[] = {
     {"force_peer_copy", 0},
     {"gpu_parse", 1},
     {"gpu_parse_block", 0},
+    {"parse_priority", 0},
     {"device_ids", 1},
     {"range_shards", 1},
     {"read_threads", 16},

@@ -27,6 +27,7 @@ enum class Opt : int {
     ForcePeerCopy,  // replicate device-built tables with cudaMemcpyPeer even on the same device
     GpuParse,       // parse LibSVM text on the GPU (1) or on host cores only (0)
     GpuParseBlock,  // GPU parser block size in bytes (0: default)
+    ParsePriority,  // GPU parser streams at the device's highest stream priority (1) or default (0)
     DeviceIds,      // keep parsed ids on the parsing GPU (1) or go through the host (0)
     RangeShards,    // text ranges per lane for multi-lane LibSVM files (0: shared reader)
     ReadThreads,    // pread threads per text block

@@ -262,8 +262,18 @@ uint64_t gpu_parse_block_bytes(uint64_t dflt) {
 
 GpuLibsvmParser::GpuLibsvmParser(int device) : device_(device) {
     BBMH_CUDA(cudaSetDevice(device));
-    BBMH_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-    BBMH_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+    // the parse kernels share the GPU with the sketch lanes' persistent
+    // kernels; at the highest stream priority their CTAs are dispatched first
+    // whenever SM slots free up (option "parse_priority")
+    int lo = 0, hi = 0;
+    if (opt(Opt::ParsePriority) && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) {
+        BBMH_CUDA(cudaStreamCreateWithPriority(&st_, cudaStreamNonBlocking, hi));
+        BBMH_CUDA(cudaStreamCreateWithPriority(&copy_st_, cudaStreamNonBlocking, hi));
+    } else {
+        cudaGetLastError();
+        BBMH_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+        BBMH_CUDA(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+    }
     BBMH_CUDA(cudaEventCreateWithFlags(&copied_, cudaEventDisableTiming));
     BBMH_CUDA(cudaMalloc(&d_flags_, 8 * sizeof(uint32_t)));
     BBMH_CUDA(cudaMallocHost(&h_flags_, 8 * sizeof(uint32_t)));
