@@ -7,18 +7,17 @@
 //             keyed_u64(seed, 8, attempt, i) >> 33 below p) is odd, else -1;
 //   a row becomes the ascending list of bins whose signed counts are non-zero,
 //   written as LibSVM text "%+d" + " %u:%g" (bin + 1, count) per entry.
-// GPU path per batch of rows: one thread per id computes the 64-bit key
-// (row << 32 | bin) and its sign; a CUB radix sort orders the keys (only the
-// bits in use), CUB reduce-by-key sums the signs per (row, bin), and the
-// non-zero entries are compacted on the device. Signed counts are exact
-// integers, so the summation order does not matter. The host formats the
-// rows in order.
+// GPU path per batch of rows (vw_row_kernel): one CTA per row hashes its ids
+// into keys bin << 1 | (sign > 0), sorts them with a bitonic network in shared
+// memory (rows longer than the shared buffer use a global scratch of the same
+// layout), and sums the signs of each run of equal bins; the non-zero runs are
+// written in bin order at the row's offset. Signed counts are exact integers,
+// so the summation order does not matter. The host formats the rows in order.
 #include <cuda_runtime.h>
 
 #include <bit>
 #include <cmath>
 #include <cstring>
-#include <cub/cub.cuh>
 #include <algorithm>
 #include <memory>
 #include <mutex>
@@ -45,45 +44,136 @@ __device__ __forceinline__ uint32_t fold31(uint32_t h, uint32_t t2, uint32_t c) 
     return (uint32_t)(v >> 32) + ((uint32_t)v >> 1);
 }
 
-__global__ void vw_keys_kernel(const uint64_t* __restrict__ row_ptr, uint64_t n,
-                               const uint32_t* __restrict__ ids, VwCoef c,
-                               unsigned long long* __restrict__ keys, int* __restrict__ vals,
-                               int* err) {
-    // one thread per row id range would serialise long rows; map threads to ids
-    // and find the row by binary search over row_ptr
-    const uint64_t total = row_ptr[n];
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t lo = 0, hi = n;  // row r with row_ptr[r] <= i < row_ptr[r+1]
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (row_ptr[mid] <= i) lo = mid;
-            else hi = mid;
-        }
-        uint32_t t = ids[i];
-        if (t >= kP31) {
-            atomicOr(err, 1);
-            t = 0;
-        }
-        const uint32_t h2 = c.a1 + c.a2 * t;
-        const uint32_t bin = c.shift ? h2 >> c.shift : h2;
-        const uint32_t t2 = t << 1;
-        uint32_t s = fold31(c.s3, t2, c.s2x2);
-        uint32_t h = min(s, s - kP31);
-        s = fold31(h, t2, c.s1x2);
-        h = min(s, s - kP31);
-        s = fold31(h, t2, c.s0x2);
-        h = min(min(s, s - kP31), s - 2 * kP31);
-        keys[i] = (unsigned long long)lo << 32 | bin;
-        vals[i] = (h & 1) ? 1 : -1;
-    }
+constexpr uint32_t kVwThreads = 256;
+constexpr uint32_t kVwSmemKeys = 8192;  // rows up to this many ids sort in shared memory
+
+__device__ __forceinline__ uint32_t vw_key(const VwCoef& c, uint32_t t) {
+    const uint32_t h2 = c.a1 + c.a2 * t;
+    const uint32_t bin = c.shift ? h2 >> c.shift : h2;  // < 2^31 for bins <= 2^31
+    const uint32_t t2 = t << 1;
+    uint32_t s = fold31(c.s3, t2, c.s2x2);
+    uint32_t h = min(s, s - kP31);
+    s = fold31(h, t2, c.s1x2);
+    h = min(s, s - kP31);
+    s = fold31(h, t2, c.s0x2);
+    h = min(min(s, s - kP31), s - 2 * kP31);
+    return bin << 1 | (h & 1);  // low bit: sign > 0
 }
 
-__global__ void vw_flag_kernel(const int* __restrict__ sums, const int* __restrict__ nrun,
-                               unsigned char* __restrict__ flags) {
-    const int n = *nrun;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        flags[i] = sums[i] != 0;
+// One CTA per row (grid-stride): keys -> bitonic sort -> signed run sums ->
+// the row's non-zero (bin, count) entries in bin order at out[row_ptr[r]..],
+// their number in counts[r]. `scratch` (row_ptr-indexed, 2x the ids) holds
+// the keys of rows longer than the shared buffer.
+__global__ void __launch_bounds__(kVwThreads) vw_row_kernel(const uint64_t* __restrict__ row_ptr,
+                                                            uint64_t n, const uint32_t* __restrict__ ids,
+                                                            VwCoef c, uint32_t* __restrict__ scratch,
+                                                            uint32_t* __restrict__ out_bins,
+                                                            int* __restrict__ out_sums,
+                                                            uint32_t* __restrict__ counts, int* err) {
+    __shared__ uint32_t s_keys[kVwSmemKeys];
+    __shared__ uint32_t s_cnt[kVwThreads];
+    const uint32_t tid = threadIdx.x;
+    for (uint64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        const uint64_t beg = row_ptr[r], end = row_ptr[r + 1];
+        const uint32_t len = (uint32_t)(end - beg);
+        uint32_t P = 1;
+        while (P < len) P <<= 1;
+        uint32_t* keys = P <= kVwSmemKeys ? s_keys : scratch + 2 * beg;
+        for (uint32_t i = tid; i < P; i += kVwThreads) {
+            uint32_t k = 0xffffffffu;  // padding sorts last
+            if (i < len) {
+                uint32_t t = ids[beg + i];
+                if (t >= kP31) {  // the reference fails here (vw.cpp:38-40); the host stops at this row
+                    atomicOr(err, 1);
+                    t = 0;
+                }
+                k = vw_key(c, t);
+            }
+            keys[i] = k;
+        }
+        __syncthreads();
+        // bitonic sort, ascending
+        for (uint32_t kk = 2; kk <= P; kk <<= 1) {
+            for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+                for (uint32_t i = tid; i < P; i += kVwThreads) {
+                    const uint32_t ixj = i ^ j;
+                    if (ixj > i) {
+                        const uint32_t a = keys[i], b = keys[ixj];
+                        const bool up = (i & kk) == 0;
+                        if ((a > b) == up) {
+                            keys[i] = b;
+                            keys[ixj] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // each thread takes a contiguous chunk of positions; a run belongs to
+        // the chunk holding its first key and is summed by walking it
+        const uint32_t chunk = (len + kVwThreads - 1) / kVwThreads;
+        const uint32_t p0 = min(len, tid * chunk), p1 = min(len, p0 + chunk);
+        auto run_sum = [&](uint32_t i, uint32_t& next) {
+            const uint32_t bin = keys[i] >> 1;
+            int sum = 0;
+            uint32_t q = i;
+            for (; q < len && (keys[q] >> 1) == bin; ++q) sum += (keys[q] & 1) ? 1 : -1;
+            next = q;
+            return sum;
+        };
+        uint32_t mine = 0;
+        for (uint32_t i = p0; i < p1;) {
+            if (i > 0 && (keys[i] >> 1) == (keys[i - 1] >> 1)) {
+                ++i;
+                continue;
+            }
+            uint32_t nx;
+            mine += run_sum(i, nx) != 0;
+            i = nx;
+        }
+        s_cnt[tid] = mine;
+        __syncthreads();
+        // exclusive scan of the per-thread counts (256: one warp per step)
+        if (tid < 32) {
+            uint32_t v[kVwThreads / 32], acc = 0;
+#pragma unroll
+            for (int w = 0; w < (int)(kVwThreads / 32); ++w) {
+                v[w] = s_cnt[tid * (kVwThreads / 32) + w];
+                acc += v[w];
+            }
+            uint32_t incl = acc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= (uint32_t)o) incl += y;
+            }
+            uint32_t run = incl - acc;
+#pragma unroll
+            for (int w = 0; w < (int)(kVwThreads / 32); ++w) {
+                const uint32_t x = v[w];
+                s_cnt[tid * (kVwThreads / 32) + w] = run;
+                run += x;
+            }
+            if (tid == 31) counts[r] = incl;
+        }
+        __syncthreads();
+        uint32_t pos = s_cnt[tid];
+        for (uint32_t i = p0; i < p1;) {
+            if (i > 0 && (keys[i] >> 1) == (keys[i - 1] >> 1)) {
+                ++i;
+                continue;
+            }
+            uint32_t nx;
+            const int sum = run_sum(i, nx);
+            if (sum != 0) {
+                out_bins[beg + pos] = keys[i] >> 1;
+                out_sums[beg + pos] = sum;
+                ++pos;
+            }
+            i = nx;
+        }
+        __syncthreads();  // keys / s_cnt are reused by the next row
+    }
 }
 
 // page-locked host array (D2H at full PCIe rate, no zero-fill of a std::vector)
@@ -186,49 +276,17 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
     };
     // buffers live for the call (the library keeps no device or page-locked
     // memory between VW calls)
-    DevBufs D;
-    auto& d_rp = D.d_rp;
-    auto& d_ids = D.d_ids;
-    auto& d_keys = D.d_keys;
-    auto& d_keys2 = D.d_keys2;
-    auto& d_ukeys = D.d_ukeys;
-    auto& d_okeys = D.d_okeys;
-    auto& d_vals = D.d_vals;
-    auto& d_vals2 = D.d_vals2;
-    auto& d_sums = D.d_sums;
-    auto& d_osums = D.d_osums;
-    auto& d_nrun = D.d_nrun;
-    auto& d_nsel = D.d_nsel;
-    auto& d_err = D.d_err;
-    auto& d_flags = D.d_flags;
-    auto& d_tmp = D.d_tmp;
-    d_nrun.reserve(1);
-    d_nsel.reserve(1);
+    Buf<uint64_t> d_rp;
+    Buf<uint32_t> d_ids, d_scratch, d_bins, d_counts;
+    Buf<int> d_sums, d_err;
     d_err.reserve(1);
-    {
-        // one allocation round for the largest batch (growing buffers batch by
-        // batch re-allocates, and cudaFree stalls)
-        const size_t cap = (1u << 24) + (1u << 22);
-        d_ids.reserve(cap);
-        d_keys.reserve(cap);
-        d_keys2.reserve(cap);
-        d_vals.reserve(cap);
-        d_vals2.reserve(cap);
-        d_ukeys.reserve(cap);
-        d_sums.reserve(cap);
-        d_okeys.reserve(cap);
-        d_osums.reserve(cap);
-        d_flags.reserve(cap);
-        d_rp.reserve((1u << 16) + 1);
-    }
-    HostBuf<unsigned long long> keys;
+    HostBuf<uint32_t> bins_h, counts_h;
     HostBuf<int> sums;
     Batch batch;
     uint64_t rows_written = 0;
     int dev = 0, sms = 148;
     BBMH_CUDA(cudaGetDevice(&dev));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int row_bits = 17, bin_bits = 32;  // rows per batch < 2^17
     for (;;) {
         batch.clear();
         batch.reserve_ids((1u << 24) + (1u << 22));
@@ -237,57 +295,31 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         trace("vw: filled");
         const uint64_t n = batch.n, nid = batch.nids();
         uint64_t n_ok = n;  // rows to write (those before a failing one)
-        int nsel = 0;
+        counts_h.reserve(n + 1);
         if (nid) {
             d_rp.reserve(n + 1);
             d_ids.reserve(nid);
-            d_keys.reserve(nid);
-            d_keys2.reserve(nid);
-            d_vals.reserve(nid);
-            d_vals2.reserve(nid);
-            d_ukeys.reserve(nid);
+            d_bins.reserve(nid);
             d_sums.reserve(nid);
-            d_okeys.reserve(nid);
-            d_osums.reserve(nid);
-            d_flags.reserve(nid);
+            d_counts.reserve(n);
+            // rows longer than the shared buffer sort in a scratch of 2x their ids
+            uint64_t longest = 0;
+            for (uint64_t r = 0; r < n; ++r) longest = std::max(longest, batch.row_ptr[r + 1] - batch.row_ptr[r]);
+            if (longest > kVwSmemKeys) d_scratch.reserve(2 * nid + 2);
             BBMH_CUDA(cudaMemcpyAsync(d_rp.p, batch.row_ptr.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
             BBMH_CUDA(cudaMemcpyAsync(d_ids.p, batch.ids, nid * 4, cudaMemcpyHostToDevice, st));
             BBMH_CUDA(cudaMemsetAsync(d_err.p, 0, sizeof(int), st));
-            const unsigned grid = (unsigned)std::min<uint64_t>((nid + 255) / 256, uint64_t(sms) * 32);
-            vw_keys_kernel<<<grid, 256, 0, st>>>(d_rp.p, n, d_ids.p, coef, d_keys.p, d_vals.p, d_err.p);
+            const unsigned grid = (unsigned)std::min<uint64_t>(n, uint64_t(sms) * 8);
+            vw_row_kernel<<<grid, kVwThreads, 0, st>>>(d_rp.p, n, d_ids.p, coef, d_scratch.p, d_bins.p,
+                                                      d_sums.p, d_counts.p, d_err.p);
             BBMH_CUDA(cudaGetLastError());
             count_launches(1);
-            const int end_bit = bin_bits + row_bits;
-            size_t need = 0, n2 = 0, n3 = 0;
-            BBMH_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, d_keys.p, d_keys2.p, d_vals.p,
-                                                      d_vals2.p, (int)nid, 0, end_bit, st));
-            BBMH_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, n2, d_keys2.p, d_ukeys.p, d_vals2.p,
-                                                     d_sums.p, d_nrun.p, cuda::std::plus<int>(),
-                                                     (int)nid, st));
-            BBMH_CUDA(cub::DeviceSelect::Flagged(nullptr, n3, d_ukeys.p, d_flags.p, d_okeys.p,
-                                                 d_nsel.p, (int)nid, st));
-            d_tmp.reserve(std::max({need, n2, n3, size_t(1)}));
-            size_t tb = d_tmp.cap;
-            BBMH_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp.p, tb, d_keys.p, d_keys2.p, d_vals.p,
-                                                      d_vals2.p, (int)nid, 0, end_bit, st));
-            tb = d_tmp.cap;
-            BBMH_CUDA(cub::DeviceReduce::ReduceByKey(d_tmp.p, tb, d_keys2.p, d_ukeys.p, d_vals2.p,
-                                                     d_sums.p, d_nrun.p, cuda::std::plus<int>(),
-                                                     (int)nid, st));
-            vw_flag_kernel<<<grid, 256, 0, st>>>(d_sums.p, d_nrun.p, d_flags.p);
-            count_launches(1);
-            // runs beyond *d_nrun carry stale flags: select over nid only after zeroing them
-            int nrun = 0;
-            BBMH_CUDA(cudaMemcpyAsync(&nrun, d_nrun.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-            BBMH_CUDA(cudaStreamSynchronize(st));
-            tb = d_tmp.cap;
-            BBMH_CUDA(cub::DeviceSelect::Flagged(d_tmp.p, tb, d_ukeys.p, d_flags.p, d_okeys.p,
-                                                 d_nsel.p, nrun, st));
-            tb = d_tmp.cap;
-            BBMH_CUDA(cub::DeviceSelect::Flagged(d_tmp.p, tb, d_sums.p, d_flags.p, d_osums.p,
-                                                 d_nsel.p, nrun, st));
             int err = 0;
-            BBMH_CUDA(cudaMemcpyAsync(&nsel, d_nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+            bins_h.reserve(nid);
+            sums.reserve(nid);
+            BBMH_CUDA(cudaMemcpyAsync(counts_h.p, d_counts.p, n * 4, cudaMemcpyDeviceToHost, st));
+            BBMH_CUDA(cudaMemcpyAsync(bins_h.p, d_bins.p, nid * 4ull, cudaMemcpyDeviceToHost, st));
+            BBMH_CUDA(cudaMemcpyAsync(sums.p, d_sums.p, nid * 4ull, cudaMemcpyDeviceToHost, st));
             BBMH_CUDA(cudaMemcpyAsync(&err, d_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
             BBMH_CUDA(cudaStreamSynchronize(st));
             if (err) {
@@ -302,13 +334,8 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
                     }
                 n_ok = bad_row;
             }
-            keys.reserve(size_t(nsel) + 1);
-            sums.reserve(size_t(nsel) + 1);
-            if (nsel) {
-                BBMH_CUDA(cudaMemcpyAsync(keys.p, d_okeys.p, nsel * 8ull, cudaMemcpyDeviceToHost, st));
-                BBMH_CUDA(cudaMemcpyAsync(sums.p, d_osums.p, nsel * 4ull, cudaMemcpyDeviceToHost, st));
-                BBMH_CUDA(cudaStreamSynchronize(st));
-            }
+        } else {
+            std::memset(counts_h.p, 0, n * 4);
         }
         trace("vw: device done");
         // write_libsvm (dataio.cpp:115-125): "%+d" then " %u:%g" per entry.
@@ -320,19 +347,19 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
         std::vector<size_t> used(T, 0);
         auto fmt = [&](unsigned w) {
             const uint64_t r0 = n_ok * w / T, r1 = n_ok * (w + 1) / T;
-            // first entry of row r0: keys are sorted by (row << 32 | bin)
-            uint64_t e = std::lower_bound(keys.p, keys.p + nsel, (unsigned long long)r0 << 32) - keys.p;
-            uint64_t e_end = std::lower_bound(keys.p, keys.p + nsel, (unsigned long long)r1 << 32) - keys.p;
+            uint64_t entries = 0;
+            for (uint64_t r = r0; r < r1; ++r) entries += counts_h.p[r];
             std::vector<char>& buf = parts[w];
-            buf.resize((e_end - e) * 24 + (r1 - r0) * 8 + 64);
+            buf.resize(entries * 24 + (r1 - r0) * 8 + 64);
             char* p = buf.data();
             for (uint64_t r = r0; r < r1; ++r) {
                 const int lab = batch.labels[r];
                 *p++ = lab < 0 ? '-' : '+';
                 p = put_uint(p, uint64_t(lab < 0 ? -lab : lab));
-                for (; e < e_end && (keys[e] >> 32) == r; ++e) {
-                    const uint32_t bin = uint32_t(keys[e]);
-                    const int v = sums[e];
+                const uint64_t e0 = batch.row_ptr[r], e1 = e0 + counts_h.p[r];
+                for (uint64_t e = e0; e < e1; ++e) {
+                    const uint32_t bin = bins_h.p[e];
+                    const int v = sums.p[e];
                     *p++ = ' ';
                     p = put_uint(p, uint32_t(bin + 1u));  // "%u" of the u32 index + 1
                     *p++ = ':';

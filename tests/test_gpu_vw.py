@@ -66,3 +66,18 @@ def test_vw_writes_the_rows_before_a_bad_id(bb, ref, tmp_path):
     r = _vw(ref.lib, ref.last_error, str(tmp_path / "head.bbcv"), str(tmp_path / "r.txt"), 1 << 12, 3)
     assert r[0] == 0
     assert (tmp_path / "g.txt").read_bytes() == (tmp_path / "r.txt").read_bytes()
+
+
+def test_vw_long_rows_use_the_global_sort(bb, ref, tmp_path):
+    """Rows longer than the kernel's shared-memory sort buffer (8,192 ids) sort
+    in global scratch: same bytes as the reference, next to short rows."""
+    rng = np.random.default_rng(6)
+    rows = []
+    for n in (5, 20_000, 0, 8_193, 8_192, 3, 40_000):
+        rows.append((1 if n % 2 else -1, np.unique(rng.integers(0, (1 << 31) - 1, n)).astype(np.uint32)))
+    (tmp_path / "c.bbcv").write_bytes(bbcv_bytes(1 << 31, rows))
+    for bins in (1, 1 << 4, 1 << 13, 1 << 31):
+        r = _vw(ref.lib, ref.last_error, str(tmp_path / "c.bbcv"), str(tmp_path / "r.txt"), bins, 5)
+        g = _vw(bb.lib(), bb.last_error, str(tmp_path / "c.bbcv"), str(tmp_path / "g.txt"), bins, 5)
+        assert r[0] == 0 and g == r, (bins, g, r)
+        assert (tmp_path / "g.txt").read_bytes() == (tmp_path / "r.txt").read_bytes(), bins
