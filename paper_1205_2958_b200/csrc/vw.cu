@@ -47,9 +47,11 @@ __device__ __forceinline__ uint32_t fold31(uint32_t h, uint32_t t2, uint32_t c) 
 constexpr uint32_t kVwThreads = 256;
 constexpr uint32_t kVwSmemKeys = 8192;  // rows up to this many ids sort in shared memory
 
-__device__ __forceinline__ uint32_t vw_key(const VwCoef& c, uint32_t t) {
+// bin << 1 | (sign > 0). A bin has up to 32 bits: with bins = 1 the 2U hash is
+// shifted by 32, which the reference's x86 build executes as a shift by 0.
+__device__ __forceinline__ unsigned long long vw_key(const VwCoef& c, uint32_t t) {
     const uint32_t h2 = c.a1 + c.a2 * t;
-    const uint32_t bin = c.shift ? h2 >> c.shift : h2;  // < 2^31 for bins <= 2^31
+    const uint32_t bin = c.shift ? h2 >> c.shift : h2;
     const uint32_t t2 = t << 1;
     uint32_t s = fold31(c.s3, t2, c.s2x2);
     uint32_t h = min(s, s - kP31);
@@ -57,7 +59,7 @@ __device__ __forceinline__ uint32_t vw_key(const VwCoef& c, uint32_t t) {
     h = min(s, s - kP31);
     s = fold31(h, t2, c.s0x2);
     h = min(min(s, s - kP31), s - 2 * kP31);
-    return bin << 1 | (h & 1);  // low bit: sign > 0
+    return (unsigned long long)bin << 1 | (h & 1);
 }
 
 // One CTA per row (grid-stride): keys -> bitonic sort -> signed run sums ->
@@ -66,11 +68,11 @@ __device__ __forceinline__ uint32_t vw_key(const VwCoef& c, uint32_t t) {
 // the keys of rows longer than the shared buffer.
 __global__ void __launch_bounds__(kVwThreads) vw_row_kernel(const uint64_t* __restrict__ row_ptr,
                                                             uint64_t n, const uint32_t* __restrict__ ids,
-                                                            VwCoef c, uint32_t* __restrict__ scratch,
+                                                            VwCoef c, unsigned long long* __restrict__ scratch,
                                                             uint32_t* __restrict__ out_bins,
                                                             int* __restrict__ out_sums,
                                                             uint32_t* __restrict__ counts, int* err) {
-    __shared__ uint32_t s_keys[kVwSmemKeys];
+    extern __shared__ unsigned long long s_keys[];  // kVwSmemKeys
     __shared__ uint32_t s_cnt[kVwThreads];
     const uint32_t tid = threadIdx.x;
     for (uint64_t r = blockIdx.x; r < n; r += gridDim.x) {
@@ -78,9 +80,9 @@ __global__ void __launch_bounds__(kVwThreads) vw_row_kernel(const uint64_t* __re
         const uint32_t len = (uint32_t)(end - beg);
         uint32_t P = 1;
         while (P < len) P <<= 1;
-        uint32_t* keys = P <= kVwSmemKeys ? s_keys : scratch + 2 * beg;
+        unsigned long long* keys = P <= kVwSmemKeys ? s_keys : scratch + 2 * beg;
         for (uint32_t i = tid; i < P; i += kVwThreads) {
-            uint32_t k = 0xffffffffu;  // padding sorts last
+            unsigned long long k = ~0ull;  // padding sorts last (above any bin << 1 | sign)
             if (i < len) {
                 uint32_t t = ids[beg + i];
                 if (t >= kP31) {  // the reference fails here (vw.cpp:38-40); the host stops at this row
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(kVwThreads) vw_row_kernel(const uint64_t* __re
                 for (uint32_t i = tid; i < P; i += kVwThreads) {
                     const uint32_t ixj = i ^ j;
                     if (ixj > i) {
-                        const uint32_t a = keys[i], b = keys[ixj];
+                        const unsigned long long a = keys[i], b = keys[ixj];
                         const bool up = (i & kk) == 0;
                         if ((a > b) == up) {
                             keys[i] = b;
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kVwThreads) vw_row_kernel(const uint64_t* __re
         const uint32_t chunk = (len + kVwThreads - 1) / kVwThreads;
         const uint32_t p0 = min(len, tid * chunk), p1 = min(len, p0 + chunk);
         auto run_sum = [&](uint32_t i, uint32_t& next) {
-            const uint32_t bin = keys[i] >> 1;
+            const unsigned long long bin = keys[i] >> 1;
             int sum = 0;
             uint32_t q = i;
             for (; q < len && (keys[q] >> 1) == bin; ++q) sum += (keys[q] & 1) ? 1 : -1;
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kVwThreads) vw_row_kernel(const uint64_t* __re
             uint32_t nx;
             const int sum = run_sum(i, nx);
             if (sum != 0) {
-                out_bins[beg + pos] = keys[i] >> 1;
+                out_bins[beg + pos] = uint32_t(keys[i] >> 1);
                 out_sums[beg + pos] = sum;
                 ++pos;
             }
@@ -277,7 +279,8 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
     // buffers live for the call (the library keeps no device or page-locked
     // memory between VW calls)
     Buf<uint64_t> d_rp;
-    Buf<uint32_t> d_ids, d_scratch, d_bins, d_counts;
+    Buf<uint32_t> d_ids, d_bins, d_counts;
+    Buf<unsigned long long> d_scratch;
     Buf<int> d_sums, d_err;
     d_err.reserve(1);
     HostBuf<uint32_t> bins_h, counts_h;
@@ -310,7 +313,12 @@ uint64_t vw_project_file(const std::string& corpus_path, const std::string& out_
             BBMH_CUDA(cudaMemcpyAsync(d_ids.p, batch.ids, nid * 4, cudaMemcpyHostToDevice, st));
             BBMH_CUDA(cudaMemsetAsync(d_err.p, 0, sizeof(int), st));
             const unsigned grid = (unsigned)std::min<uint64_t>(n, uint64_t(sms) * 8);
-            vw_row_kernel<<<grid, kVwThreads, 0, st>>>(d_rp.p, n, d_ids.p, coef, d_scratch.p, d_bins.p,
+            static const bool smem_ok = [] {
+                return cudaFuncSetAttribute(vw_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(kVwSmemKeys * sizeof(unsigned long long))) == cudaSuccess;
+            }();
+            if (!smem_ok) fail(Errc::Cuda, "cannot give the VW row kernel its shared sort buffer");
+            vw_row_kernel<<<grid, kVwThreads, kVwSmemKeys * sizeof(unsigned long long), st>>>(d_rp.p, n, d_ids.p, coef, d_scratch.p, d_bins.p,
                                                       d_sums.p, d_counts.p, d_err.p);
             BBMH_CUDA(cudaGetLastError());
             count_launches(1);
