@@ -36,6 +36,7 @@ constexpr Def kDefs[] = {
     {"parse_priority", 0},
     {"device_ids", 1},
     {"range_shards", 1},
+    {"text_lanes", 4},
     {"read_threads", 16},
     {"delta16", -1},
     {"delta_raw_every", 0},

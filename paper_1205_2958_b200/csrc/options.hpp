@@ -30,6 +30,7 @@ enum class Opt : int {
     ParsePriority,  // GPU parser streams at the device's highest stream priority (1) or default (0)
     DeviceIds,      // keep parsed ids on the parsing GPU (1) or go through the host (0)
     RangeShards,    // text ranges per lane for multi-lane LibSVM files (0: shared reader)
+    TextLanes,      // loader lanes for LibSVM text files in all (at least one per GPU)
     ReadThreads,    // pread threads per text block
     Delta16,        // 16-bit id transfer: -1 where it pays, 0 never, 1 whenever possible
     DeltaRawEvery,  // every n-th chunk crosses as 4-byte ids (0: none)

@@ -399,7 +399,12 @@ PipelineStats run_ranged(const Family& f, const std::string& path, unsigned thre
     trace("ranged: start");
     PipelineStats stats;
     const size_t cb = packed_code_bytes(f.k, b);
-    const std::vector<int> devs = pipeline_devices();
+    // lanes: the pipeline's GPUs, repeated up to the "text_lanes" loader count
+    // (several loaders per GPU overlap one range's read with another's parse)
+    const std::vector<int> gpus = pipeline_devices();
+    std::vector<int> devs;
+    const size_t nlanes = std::max<size_t>(gpus.size(), size_t(std::max<int64_t>(1, opt(Opt::TextLanes))));
+    for (size_t i = 0; i < nlanes; ++i) devs.push_back(gpus[i % gpus.size()]);
     const uint64_t max_docs = chunk_docs_setting();
     const bool b_ok = b >= 1 && b <= 32;
     const uint64_t size = file_size(path);
@@ -595,12 +600,16 @@ PipelineStats run_ranged(const Family& f, const std::string& path, unsigned thre
     return stats;
 }
 
-// Several GPUs on one LibSVM text file read it as line-aligned ranges, one
-// loader per GPU (run_ranged); "range_shards" > 1 does so on one GPU too.
+// LibSVM text files are read as line-aligned ranges by several loader lanes
+// (run_ranged): one per GPU at least, "text_lanes" in all (on one GPU, 4
+// lanes took C4 text from 29.3 to 35.2 GB/s with 2U and from 15.8 to
+// 19.3 GB/s with 4U, profiles/round2/c4_lanes_*.jsonl); "range_shards" = 0
+// keeps one shared reader.
 bool use_ranges(const std::string& path) {
     const int64_t rs = opt(Opt::RangeShards);
     if (rs <= 0) return false;
-    return (pipeline_devices().size() > 1 || rs > 1) && is_libsvm_text(path);
+    const size_t lanes = std::max<size_t>(pipeline_devices().size(), size_t(std::max<int64_t>(1, opt(Opt::TextLanes))));
+    return (lanes > 1 || rs > 1) && is_libsvm_text(path);
 }
 
 }  // namespace

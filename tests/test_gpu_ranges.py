@@ -14,10 +14,12 @@ from test_gpu_parse import _corpus
 pytestmark = pytest.mark.gpu
 
 
-def _sketch(bb, path, out, scheme=1, dim=1 << 22, k=64, b=8, devices=(0,), ranges=1, block=0):
+def _sketch(bb, path, out, scheme=1, dim=1 << 22, k=64, b=8, devices=(0,), ranges=1, block=0,
+            lanes=1):
     bb.set_devices(list(devices))
     bb.set_option("range_shards", ranges)
     bb.set_option("gpu_parse_block", block)
+    bb.set_option("text_lanes", lanes)  # loader lanes in all (>= one per device)
     try:
         with bb.Family(scheme, dim, k, 42) as f:
             try:
@@ -30,6 +32,7 @@ def _sketch(bb, path, out, scheme=1, dim=1 << 22, k=64, b=8, devices=(0,), range
         bb.set_devices([0])
         bb.set_option("range_shards", 1)
         bb.set_option("gpu_parse_block", 0)
+        bb.set_option("text_lanes", 4)
 
 
 @pytest.mark.parametrize("mixed", [False, True])
@@ -46,15 +49,17 @@ def test_ranges_byte_identical_to_one_reader_and_reference(bb, ref, tmp_path, mi
     assert s == 0
     assert one[1] == (tmp_path / "ref.bbmh").read_bytes()
     r0, b0 = bb.counter("range_shards"), bb.counter("device_id_batches")
-    for devices, ranges, block in (((0, 0, 0), 1, 0), ((0, 0, 0), 1, 1 << 15), ((0,), 4, 4099),
-                                   ((0, 0), 3, 0), ((0, 0, 0), 7, 1 << 16)):
+    for devices, ranges, block, lanes in (((0, 0, 0), 1, 0, 1), ((0, 0, 0), 1, 1 << 15, 1), ((0,), 4, 4099, 1),
+                                          ((0, 0), 3, 0, 1), ((0, 0, 0), 7, 1 << 16, 1), ((0,), 1, 0, 4),
+                                          ((0, 0), 2, 1 << 15, 4)):
         res = _sketch(bb, str(path), str(tmp_path / "r.bbmh"), devices=devices, ranges=ranges,
-                      block=block)
+                      block=block, lanes=lanes)
+        n_lanes = max(len(devices), lanes)
         assert res[0] == 0, (devices, ranges, res)
-        assert res[1] == one[1], (devices, ranges, block)
+        assert res[1] == one[1], (devices, ranges, block, lanes)
         assert res[2]["records"] == one[2]["records"]
-        assert res[3]["ranges"] == len(devices) * ranges and res[3]["lanes"] == len(devices)
-    assert bb.counter("range_shards") - r0 == 3 + 3 + 4 + 6 + 21
+        assert res[3]["ranges"] == n_lanes * ranges and res[3]["lanes"] == n_lanes
+    assert bb.counter("range_shards") - r0 == 3 + 3 + 4 + 6 + 21 + 4 + 8
     if not mixed:
         assert bb.counter("device_id_batches") > b0, "no batch kept its ids on the parsing GPU"
 
@@ -75,8 +80,9 @@ def test_ranges_report_the_first_bad_line_of_the_file(bb, ref, tmp_path, where):
     msg = ref.last_error()
     ref.destroy(h)
     assert s == one[0] and msg in one[1], (s, msg, one[1])
-    for devices, ranges in (((0, 0, 0), 1), ((0,), 5), ((0, 0), 4)):
-        res = _sketch(bb, str(path), str(tmp_path / "r.bbmh"), devices=devices, ranges=ranges)
+    for devices, ranges, lanes in (((0, 0, 0), 1, 1), ((0,), 5, 1), ((0, 0), 4, 1), ((0,), 1, 4)):
+        res = _sketch(bb, str(path), str(tmp_path / "r.bbmh"), devices=devices, ranges=ranges,
+                      lanes=lanes)
         assert res[:2] == one[:2], (devices, ranges, res[:2], one[:2])
 
 

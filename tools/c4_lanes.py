@@ -34,6 +34,7 @@ def main():
         devs = [i % ngpu for i in range(lanes)]
         bbmh.set_devices(devs)
         bbmh.set_option("range_shards", 1 if lanes > 1 else 0)
+        bbmh.set_option("text_lanes", lanes)
         with bbmh.Family(sid, dim, 500, 42) as f:
             for d in set(devs):
                 f.prepare(d)
@@ -55,6 +56,7 @@ def main():
                           "profile": best[1], "bytes_equal_one_lane": same}), flush=True)
     bbmh.set_devices([0])
     bbmh.set_option("range_shards", 1)
+    bbmh.set_option("text_lanes", 4)
 
 
 if __name__ == "__main__":
