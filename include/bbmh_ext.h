@@ -185,7 +185,8 @@ BBMH_API void bbmh_ext_replay_close(bbmh_ext_replay* replay);
 
 /* Monotonic per-process counters of which routes ran: "kernel_launches",
  * "h2d_bytes", "d2h_bytes", "peer_copy_bytes", "zero_copy_calls",
- * "delta16_chunks", "raw_chunks", "range_shards", "device_id_batches". */
+ * "delta16_chunks", "raw_chunks", "range_shards", "device_id_batches",
+ * "uniform_launches". */
 BBMH_API bbmh_status bbmh_ext_counter(const char* name, uint64_t* value_out);
 
 /* Permutation table j (dim u32 values, the reference's perm_[j*D .. j*D+D),

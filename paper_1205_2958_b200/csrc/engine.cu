@@ -179,6 +179,7 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device,
         BBMH_CUDA(cudaMemcpy(df->d_coef, coef.data(), coef.size() * sizeof(uint32_t),
                              cudaMemcpyHostToDevice));
         kf.coef = df->d_coef;
+        if (scheme == Scheme::TwoU) kf.host2u = f.twou.data();  // lives as long as f (and df)
     }
     if (f.scheme == Scheme::Permutation) {
         const size_t bytes = size_t(f.dim) * f.k * sizeof(uint32_t);

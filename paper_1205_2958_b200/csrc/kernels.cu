@@ -754,6 +754,9 @@ void dispatch_split(const KernelFamily& F, const uint64_t* row_ptr, uint64_t bas
 
 }  // namespace
 
+int sm_count() { return device_sms(); }
+unsigned long long* ticket_slot(int dev) { return work_slot(dev); }
+
 LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     // Each thread owns J hash functions and streams every staged id, so its
     // serial work is ~J * eff per id, where eff is the measured relative
@@ -834,6 +837,7 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
     const LaunchShape sh = choose_shape(F.k, F.scheme, n, device_sms());
     switch (F.scheme) {
         case S_2U:
+            if (launch_uniform_2u(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st)) return;
             return dispatch_j<S_2U, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         case S_4UBIT:
             if (F.dim_pow2)
@@ -873,7 +877,8 @@ void transfer_counts(uint64_t& h2d, uint64_t& d2h) {
 namespace {
 std::atomic<uint64_t> g_counters[int(Counter::kCount)];
 constexpr const char* kCounterNames[] = {"peer_copy_bytes", "zero_copy_calls", "delta16_chunks",
-                                         "raw_chunks", "range_shards", "device_id_batches"};
+                                         "raw_chunks", "range_shards", "device_id_batches",
+                                         "uniform_launches"};
 static_assert(sizeof(kCounterNames) / sizeof(kCounterNames[0]) == size_t(Counter::kCount));
 }  // namespace
 

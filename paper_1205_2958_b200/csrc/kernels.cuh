@@ -25,6 +25,7 @@ struct KernelFamily {
     uint64_t barrett = 0;    // 4U-mod: floor((2^64 - 1) / p)
     const uint32_t* coef = nullptr;  // 2U: k*{a1,a2}; 4U-bit: k*{a3,2a2,2a1,2a0}; 4U-mod: k*{a3,a2,a1,a0}
     const uint32_t* perm = nullptr;  // permutation tables, k*dim
+    const uint32_t* host2u = nullptr;  // 2U: the family's host k*{a1,a2} (uniform kernel parameters)
 };
 
 struct LaunchShape {
@@ -60,6 +61,17 @@ void launch_score(const uint8_t* codes, const uint8_t* flags, uint64_t n, uint32
                   const double* w, uint64_t wdim, double* scores, unsigned long long* bad,
                   cudaStream_t stream);
 
+// 2U with 32 < k <= 544 over >= kUniformMinDocs documents: the
+// coefficient-uniform kernel (uniform.cu). false: it does not apply.
+bool launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
+                       const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
+                       uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
+
+// SM count of the current device (cached) and a zeroed {ticket, exit}
+// counter pair for one launch (nullptr: none could be allocated).
+int sm_count();
+unsigned long long* ticket_slot(int dev);
+
 uint64_t kernel_launch_count();
 void count_launches(uint64_t n);
 
@@ -76,13 +88,14 @@ enum class Counter : int {
     RawChunks,       // host chunks whose ids crossed as 4-byte ids (or were device-resident)
     RangeShards,     // LibSVM text ranges sketched by range-sharded lanes
     DeviceIdBatches, // loader batches whose ids never left the parsing GPU
+    UniformLaunches, // 2U launches of the coefficient-uniform kernel (uniform.cu)
     kCount
 };
 void count(Counter c, uint64_t n = 1);
 inline void count_peer_copy(uint64_t bytes) { count(Counter::PeerCopyBytes, bytes); }
 // by name: "kernel_launches", "h2d_bytes", "d2h_bytes", "peer_copy_bytes",
 // "zero_copy_calls", "delta16_chunks", "raw_chunks", "range_shards",
-// "device_id_batches"; false if unknown
+// "device_id_batches", "uniform_launches"; false if unknown
 bool counter_value(const char* name, uint64_t* out);
 
 }  // namespace bbmh

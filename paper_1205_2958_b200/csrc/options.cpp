@@ -27,6 +27,8 @@ constexpr Def kDefs[] = {
     {"carveout", -1},
     {"dynamic_docs", 1},
     {"split_small_k", 1},
+    {"uniform_2u", 1},
+    {"uniform_sb_docs", 0},
     {"perm_tablewise", -1},
     {"perm_scratch_mb", 2048},
     {"gpu_permgen", 1},
