@@ -638,7 +638,7 @@ void Lane::enqueue_packed(Slot& s, const ChunkJob& job, uint64_t nidx) {
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
     launch_sketch(df_->kf, reinterpret_cast<const uint64_t*>(d), job.index_base, d_ids, n, b_,
                   d + s.off_codes,
-                  nullptr, d + s.off_flags, d_err, s.st);
+                  nullptr, d + s.off_flags, d_err, s.st, n ? double(nidx) / double(n) : 0.0);
     BBMH_CUDA(cudaGetLastError());
     if (d_w_) {
         launch_score(d + s.off_codes, d + s.off_flags, n, f_.k, b_, d_w_, wdim_,
@@ -685,7 +685,8 @@ void Lane::enqueue(Slot& s, const ChunkJob& job) {
     BBMH_CUDA(cudaMemsetAsync(s.d_err, 0, sizeof(int), s.st));
     if (timed_) BBMH_CUDA(cudaEventRecord(s.ev0, s.st));
     launch_sketch(df_->kf, s.d_rp, job.index_base, job.d_indices ? job.d_indices : s.d_idx, n, b_, s.d_codes,
-                  want_minima_ ? s.d_min : nullptr, s.d_flags, s.d_err, s.st);
+                  want_minima_ ? s.d_min : nullptr, s.d_flags, s.d_err, s.st,
+                  n ? double(nidx) / double(n) : 0.0);
     BBMH_CUDA(cudaGetLastError());
     if (d_w_) {  // fused scoring on the device-resident codes (score.cu)
         BBMH_CUDA(cudaMemsetAsync(s.d_bad, 0xff, sizeof(unsigned long long), s.st));
@@ -809,7 +810,7 @@ bool sketch_rows_zero_copy(const Family& f, int dev, const uint64_t* row_ptr,
     // decreasing row_ptr (rejected on the host before we get here)
     launch_sketch(df.kf, reinterpret_cast<const uint64_t*>(h), 0,
                   static_cast<const uint32_t*>(d_ids), n, b, h + off_codes, nullptr,
-                  h + off_flags, s->d_err, s->st);
+                  h + off_flags, s->d_err, s->st, n ? double(row_ptr[n] - row_ptr[0]) / double(n) : 0.0);
     BBMH_CUDA(cudaGetLastError());
     BBMH_CUDA(cudaStreamSynchronize(s->st));
     count_transfer((n + 1) * sizeof(uint64_t) + (row_ptr[n] - row_ptr[0]) * sizeof(uint32_t), n + n * cb);

@@ -248,6 +248,8 @@ __global__ void __launch_bounds__(256) sketch_kernel(KernelFamily F, const uint6
     __shared__ __align__(8) uint64_t mbar[2];
     __shared__ Item desc[2];
 
+    if (F.yield_nnz && row_ptr[n_docs] - row_ptr[0] >= (uint64_t)F.yield_nnz * n_docs)
+        return;  // the uniform kernel launched beside this one takes the batch
     const uint32_t tid = threadIdx.x;
     const uint32_t tpb = blockDim.x;
     const uint32_t k = F.k;
@@ -818,7 +820,7 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
 
 void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
                    const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes, uint64_t* minima,
-                   uint8_t* flags, int* err, cudaStream_t st) {
+                   uint8_t* flags, int* err, cudaStream_t st, double avg_nnz) {
     if (n == 0) return;
     const uint32_t split_max = F.scheme == S_2U ? 32u : 16u;  // functions a lane holds in registers
     if (F.k <= split_max && F.scheme != S_PERM && opt(Opt::SplitSmallK)) {
@@ -836,9 +838,20 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
     }
     const LaunchShape sh = choose_shape(F.k, F.scheme, n, device_sms());
     switch (F.scheme) {
-        case S_2U:
-            if (launch_uniform_2u(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st)) return;
-            return dispatch_j<S_2U, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        case S_2U: {
+            const uint32_t need = uniform_min_nnz(F, n);
+            if (!need) return dispatch_j<S_2U, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            if (avg_nnz >= 0) {
+                if (avg_nnz >= need)
+                    return launch_uniform_2u(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st, 0);
+                return dispatch_j<S_2U, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            }
+            // row lengths unknown on the host: both kernels, one returns at once
+            launch_uniform_2u(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st, need);
+            KernelFamily Fy = F;
+            Fy.yield_nnz = need;
+            return dispatch_j<S_2U, true>(Fy, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+        }
         case S_4UBIT:
             if (F.dim_pow2)
                 return dispatch_j<S_4UBIT, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);

@@ -26,6 +26,10 @@ struct KernelFamily {
     const uint32_t* coef = nullptr;  // 2U: k*{a1,a2}; 4U-bit: k*{a3,2a2,2a1,2a0}; 4U-mod: k*{a3,a2,a1,a0}
     const uint32_t* perm = nullptr;  // permutation tables, k*dim
     const uint32_t* host2u = nullptr;  // 2U: the family's host k*{a1,a2} (uniform kernel parameters)
+    // set per launch: the persistent sketch kernel returns at once when the
+    // batch averages >= yield_nnz ids per document (the uniform kernel,
+    // launched beside it, takes such batches; see launch_sketch)
+    uint32_t yield_nnz = 0;
 };
 
 struct LaunchShape {
@@ -43,9 +47,14 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n = 0, int sms = 148);
 // row_ptr values are offsets into `indices` after subtracting index_base.
 // err (device int) receives bit 1 for a permutation id >= dim and bit 2
 // for a decreasing row_ptr.
+// avg_nnz: ids per document of the batch when the caller knows it (host
+// row_ptr), < 0 when not (device row_ptr): then a 2U batch the uniform
+// kernel may take launches both 2U kernels and the batch's own row_ptr
+// decides on the device which one works.
 void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
                    const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
-                   uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
+                   uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream,
+                   double avg_nnz = -1.0);
 
 // Permutation mode with tables too large for L2: table-outer passes (perm.cu).
 bool perm_tablewise_applies(const KernelFamily& F, uint64_t n);
@@ -61,11 +70,16 @@ void launch_score(const uint8_t* codes, const uint8_t* flags, uint64_t n, uint32
                   const double* w, uint64_t wdim, double* scores, unsigned long long* bad,
                   cudaStream_t stream);
 
-// 2U with 32 < k <= 544 over >= kUniformMinDocs documents: the
-// coefficient-uniform kernel (uniform.cu). false: it does not apply.
-bool launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
+// The coefficient-uniform 2U kernel (uniform.cu) for 32 < k <= 544 over
+// >= 2,048 documents. uniform_min_nnz: the average row length from which it
+// beats the persistent kernel for this batch (0: it does not apply).
+// launch_uniform_2u with min_nnz > 0 returns on the device when the batch
+// averages fewer ids per document.
+uint32_t uniform_min_nnz(const KernelFamily& F, uint64_t n);
+void launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
                        const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
-                       uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
+                       uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream,
+                       uint32_t min_nnz);
 
 // SM count of the current device (cached) and a zeroed {ticket, exit}
 // counter pair for one launch (nullptr: none could be allocated).

@@ -71,61 +71,90 @@ struct UniformArgs {
     uint32_t groups;           // full + (tail group ? 1 : 0)
     uint32_t tail_fc;          // compile-time width of the tail body (multiple of 4; 0: none)
     uint32_t sb_docs;          // documents per super-block
+    uint32_t min_nnz;          // > 0: return unless the batch averages >= min_nnz ids per document
 };
 
 __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) {
     return min(min(a, b), c);
 }
 
-// The hot loop of an item: full steps of 64 quads (8 ids per lane, the next
-// step's loads in flight) for the functions at parameter slot S (S = g for
-// full groups, kFullGroups for the tail group of width FC). Only this loop
-// is instantiated per group, so the instruction cache holds the one or two
-// groups in flight plus the shared rest of the item.
+// The hashing of an item, for the functions at parameter slot S (S = g for
+// full groups, kFullGroups for the tail group of width FC): full steps of 64
+// quads (8 ids per lane, the next step's loads in flight), then 4-id steps
+// while they are mostly full (duplicated quads leave the minimum unchanged),
+// then single-id rounds over the remaining quads' ids, the head ids and the
+// tail ids. Only this part is instantiated per group; the instruction cache
+// holds the one or two groups in flight plus the shared epilogue.
 template <int S, int FC>
-__device__ __forceinline__ void group_steps(const UniformCoef& C, const uint4* __restrict__ q4,
-                                            uint64_t full_end, uint32_t lane, uint32_t (&m)[kGroup]) {
+__device__ __forceinline__ void group_hash(const UniformCoef& C, const uint32_t* __restrict__ ids,
+                                          uint32_t head, uint64_t nq, uint64_t nnz, uint32_t lane,
+                                          uint32_t (&m)[kGroup]) {
+    const uint4* q4 = reinterpret_cast<const uint4*>(ids + head);
     uint32_t a1[FC];
 #pragma unroll
     for (int r = 0; r < FC; ++r) a1[r] = C.a1[S * kGroup + r];
-    uint4 x = __ldg(q4 + lane), y = __ldg(q4 + 32 + lane);
-    for (uint64_t s = 0; s < full_end; s += 64) {
-        const uint4 xc = x, yc = y;
-        if (s + 64 < full_end) {
-            x = __ldg(q4 + s + 64 + lane);
-            y = __ldg(q4 + s + 96 + lane);
+    const uint64_t full_end = nq & ~63ull;
+    if (full_end) {
+        uint4 x = __ldg(q4 + lane), y = __ldg(q4 + 32 + lane);
+        for (uint64_t s = 0; s < full_end; s += 64) {
+            const uint4 xc = x, yc = y;
+            if (s + 64 < full_end) {
+                x = __ldg(q4 + s + 64 + lane);
+                y = __ldg(q4 + s + 96 + lane);
+            }
+#pragma unroll
+            for (int r = 0; r < FC; ++r) {
+                // two independent min3 chains per function: the fastest of 24
+                // reduction shapes measured (tools/proto/uni_search.cu)
+                const uint32_t a2 = C.a2[S * kGroup + r];
+                const uint32_t t0 = min3u(a1[r] + a2 * xc.y, m[r], a1[r] + a2 * yc.x);
+                const uint32_t t1 = min3u(a1[r] + a2 * xc.w, a1[r] + a2 * xc.z, a1[r] + a2 * yc.y);
+                const uint32_t t2 = min3u(a1[r] + a2 * xc.x, a1[r] + a2 * yc.w, t0);
+                m[r] = min3u(t2, t1, a1[r] + a2 * yc.z);
+            }
         }
+    }
+    uint64_t s = full_end;
+    while (nq - s > 24) {
+        const uint4 x = __ldg(q4 + min(s + lane, nq - 1));
 #pragma unroll
         for (int r = 0; r < FC; ++r) {
-            // two independent min3 chains per function: the fastest of 24
-            // reduction shapes measured (tools/proto/uni_search.cu)
             const uint32_t a2 = C.a2[S * kGroup + r];
-            const uint32_t t0 = min3u(a1[r] + a2 * xc.y, m[r], a1[r] + a2 * yc.x);
-            const uint32_t t1 = min3u(a1[r] + a2 * xc.w, a1[r] + a2 * xc.z, a1[r] + a2 * yc.y);
-            const uint32_t t2 = min3u(a1[r] + a2 * xc.x, a1[r] + a2 * yc.w, t0);
-            m[r] = min3u(t2, t1, a1[r] + a2 * yc.z);
+            const uint32_t t0 = min3u(a1[r] + a2 * x.x, a1[r] + a2 * x.y, a1[r] + a2 * x.z);
+            m[r] = min3u(m[r], t0, a1[r] + a2 * x.w);
         }
+        s = min(s + 32, nq);
+    }
+    const uint64_t rest0 = head + 4 * s;  // first unprocessed id after the head
+    const uint64_t e = head + (nnz - rest0);
+    for (uint64_t i0 = 0; i0 < e; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const uint32_t t = __ldg(ids + (i >= e ? 0 : i < head ? i : rest0 + (i - head)));
+#pragma unroll
+        for (int r = 0; r < FC; ++r) m[r] = min(m[r], a1[r] + C.a2[S * kGroup + r] * t);
     }
 }
 
 template <int G>
-__device__ __forceinline__ void steps_full(const UniformCoef& C, uint32_t g, const uint4* q4,
-                                           uint64_t full_end, uint32_t lane, uint32_t (&m)[kGroup]) {
-    if (g == G) return group_steps<G, kGroup>(C, q4, full_end, lane, m);
-    if constexpr (G + 1 < kFullGroups) steps_full<G + 1>(C, g, q4, full_end, lane, m);
+__device__ __forceinline__ void hash_full(const UniformCoef& C, uint32_t g, const uint32_t* ids,
+                                          uint32_t head, uint64_t nq, uint64_t nnz, uint32_t lane,
+                                          uint32_t (&m)[kGroup]) {
+    if (g == G) return group_hash<G, kGroup>(C, ids, head, nq, nnz, lane, m);
+    if constexpr (G + 1 < kFullGroups) hash_full<G + 1>(C, g, ids, head, nq, nnz, lane, m);
 }
 
-__device__ __forceinline__ void steps_tail(const UniformCoef& C, uint32_t fc, const uint4* q4,
-                                           uint64_t full_end, uint32_t lane, uint32_t (&m)[kGroup]) {
+__device__ __forceinline__ void hash_tail(const UniformCoef& C, uint32_t fc, const uint32_t* ids,
+                                          uint32_t head, uint64_t nq, uint64_t nnz, uint32_t lane,
+                                          uint32_t (&m)[kGroup]) {
     switch (fc) {
-        case 4: return group_steps<kFullGroups, 4>(C, q4, full_end, lane, m);
-        case 8: return group_steps<kFullGroups, 8>(C, q4, full_end, lane, m);
-        case 12: return group_steps<kFullGroups, 12>(C, q4, full_end, lane, m);
-        case 16: return group_steps<kFullGroups, 16>(C, q4, full_end, lane, m);
-        case 20: return group_steps<kFullGroups, 20>(C, q4, full_end, lane, m);
-        case 24: return group_steps<kFullGroups, 24>(C, q4, full_end, lane, m);
-        case 28: return group_steps<kFullGroups, 28>(C, q4, full_end, lane, m);
-        default: return group_steps<kFullGroups, 32>(C, q4, full_end, lane, m);
+        case 4: return group_hash<kFullGroups, 4>(C, ids, head, nq, nnz, lane, m);
+        case 8: return group_hash<kFullGroups, 8>(C, ids, head, nq, nnz, lane, m);
+        case 12: return group_hash<kFullGroups, 12>(C, ids, head, nq, nnz, lane, m);
+        case 16: return group_hash<kFullGroups, 16>(C, ids, head, nq, nnz, lane, m);
+        case 20: return group_hash<kFullGroups, 20>(C, ids, head, nq, nnz, lane, m);
+        case 24: return group_hash<kFullGroups, 24>(C, ids, head, nq, nnz, lane, m);
+        case 28: return group_hash<kFullGroups, 28>(C, ids, head, nq, nnz, lane, m);
+        default: return group_hash<kFullGroups, 32>(C, ids, head, nq, nnz, lane, m);
     }
 }
 
@@ -143,44 +172,14 @@ __device__ __forceinline__ void uniform_item(const UniformCoef& C, const Uniform
     const uint64_t h16 = ((16 - ((uintptr_t)ids & 15)) & 15) >> 2;
     const uint32_t head = (uint32_t)(nnz < h16 ? nnz : h16);
     const uint64_t nq = (nnz - head) >> 2;
-    const uint4* q4 = reinterpret_cast<const uint4*>(ids + head);
 
     uint32_t m[kGroup];
 #pragma unroll
     for (int r = 0; r < kGroup; ++r) m[r] = 0xffffffffu;
-    const uint64_t full_end = nq & ~63ull;
-    if (full_end) {
-        if (g < A.full)
-            steps_full<0>(C, g, q4, full_end, lane, m);
-        else
-            steps_tail(C, A.tail_fc, q4, full_end, lane, m);
-    }
-
-    // the rest, with the group's coefficients read by a runtime slot index:
-    // 4-id steps while they are mostly full (duplicated quads leave the
-    // minimum unchanged), then single-id rounds over the remaining quads'
-    // ids, the head ids and the tail ids (padded tail functions have zero
-    // coefficients; their minima are dropped)
-    const uint32_t slot = (g < A.full ? g : (uint32_t)kFullGroups) * kGroup;
-    uint64_t s = full_end;
-    while (nq - s > 24) {
-        const uint4 x = __ldg(q4 + min(s + lane, nq - 1));
-#pragma unroll
-        for (int r = 0; r < kGroup; ++r) {
-            const uint32_t a1 = C.a1[slot + r], a2 = C.a2[slot + r];
-            m[r] = min3u(m[r], a1 + a2 * x.x, a1 + a2 * x.y);
-            m[r] = min3u(m[r], a1 + a2 * x.z, a1 + a2 * x.w);
-        }
-        s = min(s + 32, nq);
-    }
-    const uint64_t rest0 = head + 4 * s;  // first unprocessed id after the head
-    const uint64_t e = head + (nnz - rest0);
-    for (uint64_t i0 = 0; i0 < e; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        const uint32_t t = __ldg(ids + (i >= e ? 0 : i < head ? i : rest0 + (i - head)));
-#pragma unroll
-        for (int r = 0; r < kGroup; ++r) m[r] = min(m[r], C.a1[slot + r] + C.a2[slot + r] * t);
-    }
+    if (g < A.full)
+        hash_full<0>(C, g, ids, head, nq, nnz, lane, m);
+    else
+        hash_tail(C, A.tail_fc, ids, head, nq, nnz, lane, m);
 
     // lane l ends with the warp's minimum of function l of the group
 #pragma unroll
@@ -231,6 +230,8 @@ __device__ __forceinline__ void uniform_item(const UniformCoef& C, const Uniform
 __global__ void __launch_bounds__(kTpb) sketch_uniform_kernel(const __grid_constant__ UniformCoef C,
                                                               const __grid_constant__ UniformArgs A) {
     __shared__ uint32_t s_code[kTpb / 32][kGroup];
+    if (A.min_nnz && A.row_ptr[A.n] - A.row_ptr[0] < (uint64_t)A.min_nnz * A.n)
+        return;  // the persistent kernel launched beside this one takes the batch
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = kTpb / 32;
     const uint32_t items = A.n * A.groups;
     const uint32_t stride = gridDim.x * W;
@@ -266,16 +267,29 @@ __global__ void __launch_bounds__(kTpb) sketch_uniform_kernel(const __grid_const
 
 }  // namespace
 
-bool launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
-                       const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
-                       uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st) {
-    if (F.scheme != 1 || !F.host2u || !opt(Opt::Uniform2U)) return false;
+// Measured crossovers against the persistent kernel (profiles/round2/
+// uniform_ab.jsonl, webspam-shaped rows of 40..3,728 ids): the uniform
+// kernel's per-item cost (cross-lane transpose, epilogue, partial steps) is
+// paid per (document, group), so it needs longer rows as k grows.
+uint32_t uniform_min_nnz(const KernelFamily& F, uint64_t n) {
+    const int64_t mode = opt(Opt::Uniform2U);  // 0 off, 1 by row length, 2 whenever it applies
     const uint32_t k = F.k;
-    if (k <= kGroup || k > kUniformMaxK || n < kUniformMinDocs) return false;
+    if (F.scheme != 1 || !F.host2u || mode == 0) return 0;
+    if (k <= kGroup || k > kUniformMaxK || n < kUniformMinDocs) return 0;
+    const uint32_t groups = (k + kGroup - 1) / kGroup;
+    if (n * groups >= (1ull << 32)) return 0;
+    if (mode >= 2) return 1;
+    return k <= 64 ? 700 : k <= 128 ? 1000 : k <= 300 ? 1500 : 2600;
+}
+
+void launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
+                       const uint32_t* idx, uint64_t n, uint32_t b, uint8_t* codes,
+                       uint64_t* minima, uint8_t* flags, int* err, cudaStream_t st,
+                       uint32_t min_nnz) {
+    const uint32_t k = F.k;
     const uint32_t full = std::min<uint32_t>(k / kGroup, kFullGroups);
     const uint32_t rem = k - full * kGroup;  // <= 32
     const uint32_t groups = full + (rem ? 1 : 0);
-    if (n * groups >= (1ull << 32)) return false;
 
     UniformCoef C;
     std::memset(&C, 0, sizeof(C));  // padded tail functions hash to 0; their codes are dropped
@@ -325,12 +339,12 @@ bool launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t 
     if (opt(Opt::UniformSbDocs) > 0) sb_override = (uint64_t)opt(Opt::UniformSbDocs);
     const uint64_t sb = sb_override ? sb_override : kSbDocs;
     A.sb_docs = (uint32_t)std::min<uint64_t>(sb, n);
+    A.min_nnz = min_nnz;
     sketch_uniform_kernel<<<(unsigned)grid, kTpb, 0, st>>>(C, A);
     if (const cudaError_t e = cudaPeekAtLastError(); e != cudaSuccess)
         fprintf(stderr, "bbmh: uniform 2U launch failed (%s)\n", cudaGetErrorString(e));
     count_launches(1);
     count(Counter::UniformLaunches);
-    return true;
 }
 
 }  // namespace bbmh

@@ -41,7 +41,7 @@ def test_uniform_matches_oracle(bb, port, k):
     rp, idx = _ragged(rng, n, dim)
     seed = int(rng.integers(0, 2**63))
     b = int(rng.integers(1, 33))
-    bb.set_option("uniform_2u", 1)
+    bb.set_option("uniform_2u", 2)  # whenever it applies (1: by row length)
     f = bb.Family(1, dim, k, seed)
     u0 = bb.counter("uniform_launches")
     codes, minima, flags = f.sketch_csr(rp, idx, b, want_minima=True)
@@ -56,6 +56,7 @@ def test_uniform_matches_oracle(bb, port, k):
     assert np.array_equal(flags, f2)
     port.destroy(h)
     f.close()
+    bb.set_option("uniform_2u", 1)
 
 
 @pytest.mark.parametrize("b", [1, 2, 3, 5, 7, 8, 9, 16, 24, 31, 32])
@@ -63,6 +64,7 @@ def test_uniform_every_b(bb, port, b):
     rng = np.random.default_rng(77 + b)
     dim, k = 1 << 20, 200
     rp, idx = _ragged(rng, 2100, dim)
+    bb.set_option("uniform_2u", 2)
     f = bb.Family(1, dim, k, 4242)
     codes, minima, flags = f.sketch_csr(rp, idx, b, want_minima=True)
     st, h = port.family(1, dim, k, 4242, 0, 1 << 30)
@@ -70,23 +72,29 @@ def test_uniform_every_b(bb, port, b):
     assert s == 0
     assert np.array_equal(codes, c2) and np.array_equal(minima, m2) and np.array_equal(flags, f2), b
     port.destroy(h)
+    bb.set_option("uniform_2u", 1)
 
 
 @pytest.mark.parametrize("dim", [1, 2, 1 << 31, 1 << 32])
 def test_uniform_universe_limits(bb, port, dim):
     rng = np.random.default_rng(dim % 1000)
     rp, idx = random_csr(rng, 2048, min(dim, 1 << 32), 0, 400, empty_every=5)
+    bb.set_option("uniform_2u", 2)
     f = bb.Family(1, dim, 96, 99)
     codes, minima, flags = f.sketch_csr(rp, idx, 8, want_minima=True)
     st, h = port.family(1, dim, 96, 99, 0, 1 << 30)
     s, c2, m2, f2 = port.sketch_csr(h, 96, rp, idx, 8)
     assert np.array_equal(codes, c2) and np.array_equal(minima, m2) and np.array_equal(flags, f2)
     port.destroy(h)
+    bb.set_option("uniform_2u", 1)
 
 
 def test_uniform_equals_persistent_on_device(bb):
-    """Same device batch (index base, sliced row_ptr), both kernels: identical
-    codes, minima and flags for webspam-shaped rows."""
+    """Same device batch (misaligned row starts, empty last rows), both
+    kernels: identical codes, minima and flags for webspam-shaped rows. With
+    device row_ptr the library launches both kernels and the batch's row
+    lengths pick one on the device (uniform_2u = 1); 0 runs the persistent
+    kernel alone."""
     import torch
     dev = torch.device("cuda", 0)
     n, nnz, k, b = 6000, 3728, 500, 8
@@ -109,7 +117,39 @@ def test_uniform_equals_persistent_on_device(bb):
                             flags.data_ptr(), index_base=0)
         torch.cuda.synchronize()
         assert (bb.counter("uniform_launches") - u0) == uni
+        if uni:
+            bb.set_option("uniform_2u", 2)  # the uniform kernel alone
+            codes2 = torch.zeros_like(codes)
+            f.sketch_csr_device(rp.data_ptr(), ids.data_ptr(), n, b, codes2.data_ptr(), stream=None)
+            torch.cuda.synchronize()
+            assert torch.equal(codes2, codes)
+            bb.set_option("uniform_2u", 1)
         out[uni] = (codes.cpu(), mins.cpu(), flags.cpu())
     bb.set_option("uniform_2u", 1)
     for a, c in zip(out[1], out[0]):
         assert torch.equal(a, c)
+
+
+def test_short_rows_on_device_take_the_persistent_kernel(bb):
+    """Device batch of short rows (~100 ids): under the default rule the
+    persistent kernel takes it on the device; all three modes agree."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n, k, b = 3000, 200, 8
+    g = torch.Generator(device=dev)
+    g.manual_seed(9)
+    lens = torch.randint(0, 200, (n,), generator=g, device=dev)
+    rp = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    rp[1:] = torch.cumsum(lens, 0)
+    ids = torch.randint(0, 1 << 24, (int(rp[-1].item()) + 16,), generator=g, device=dev,
+                        dtype=torch.int64).to(torch.int32)
+    f = bb.Family(1, 1 << 24, k, 5)
+    outs = []
+    for mode in (1, 0, 2):
+        bb.set_option("uniform_2u", mode)
+        codes = torch.zeros(n * k, dtype=torch.uint8, device=dev)
+        f.sketch_csr_device(rp.data_ptr(), ids.data_ptr(), n, b, codes.data_ptr())
+        torch.cuda.synchronize()
+        outs.append(codes.cpu())
+    bb.set_option("uniform_2u", 1)
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])

@@ -15,7 +15,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_1205_2958_b200 import bbmh  # noqa: E402
 
-DEFAULTS = {"uniform_2u": 1, "uniform_sb_docs": 0}
+DEFAULTS = {"uniform_2u": 2, "uniform_sb_docs": 0}
 
 
 def main():
@@ -25,7 +25,7 @@ def main():
     bs = [int(x) for x in os.environ.get("AB_BS", "8").split(",")]
     reps = int(os.environ.get("AB_REPS", "5"))
     dim = int(os.environ.get("AB_DIM", bench.D_2U))
-    arms = [{"uniform_2u": 0}] + json.loads(os.environ.get("AB_ARMS", '[{"uniform_2u": 1}]'))
+    arms = [{"uniform_2u": 0}] + json.loads(os.environ.get("AB_ARMS", "[{\"uniform_2u\": 2}]"))
     dev = torch.device("cuda", 0)
     d_rp, d_idx = bench.make_corpus_device(torch, n, nnz, dim, 1, dev)
     st = torch.cuda.current_stream()
