@@ -22,7 +22,7 @@ enum class Opt : int {
     DynamicDocs,    // small-k sketch kernel takes documents from a ticket counter (1) or round-robin (0)
     SplitSmallK,    // small-k lane-split kernel (1) or the persistent kernel (0)
     Uniform2U,      // 2U with 32 < k <= 544: coefficient-uniform kernel by row length (1), always (2), never (0)
-    UniformSbDocs,  // uniform kernel: documents per super-block (0: 16,384)
+    UniformSbDocs,  // uniform kernel: documents per super-block (0: 64 MB of ids, >= 3,072)
     PermTablewise,  // permutation schedule: -1 auto, 0 document-outer, 1 table-outer
     PermScratchMb,  // table-outer schedule: device scratch budget per pass group (MiB)
     GpuPermgen,     // build large permutation tables on the GPU (1) or the host (0)

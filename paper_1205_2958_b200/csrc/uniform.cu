@@ -16,11 +16,13 @@
 //     coefficients at fixed constant-bank offsets; the tail group (k not a
 //     multiple of 32) sits in a fixed extra slot with a compile-time width;
 //   * items come from a ticket counter in group-major order inside
-//     super-blocks of 16,384 documents, so the warps in flight run the hot
-//     loops of one or two groups: only the hot loop is instantiated per
-//     group (~7 KB each) and the instruction cache (L1.5 ~32 KB) holds a few
-//     of them -- with groups interleaved the kernel ran 40% slower on
-//     instruction-fetch stalls (ncu no_instruction, profiles/round2);
+//     super-blocks of documents that stay in L2 (each document is read from
+//     HBM about once although every group reads it) and that are larger
+//     than the items in flight, so the warps run the hot loops of one or two
+//     groups: only the hot loop is instantiated per group (~7 KB each) and
+//     the instruction cache (L1.5 ~32 KB) holds a few of them -- with
+//     groups interleaved the kernel ran 40% slower on instruction-fetch
+//     stalls (ncu no_instruction, profiles/round2);
 //   * at the end of an item the 32 lanes' partial minima are transposed and
 //     reduced with shuffles (lane l ends with function l of the group), and
 //     the b-bit codes go into the reference's bitstream (sketch.cpp:64-69).
@@ -43,12 +45,14 @@ constexpr int kFullGroups = 16;   // compile-time group bodies; the tail group u
 constexpr uint32_t kUniformMaxK = (kFullGroups + 1) * kGroup;  // 544
 // below this the persistent kernel's shorter tail wins (k = 500, 1,024 docs: 0.16 vs 0.20 ms)
 constexpr uint64_t kUniformMinDocs = 2048;
-// documents per super-block: with smaller ones the warps in flight span several
-// groups and their hot loops no longer fit the instruction cache (512 docs:
-// 6.3 T evals/s, 1,776: 11.5 T, >= 8,192: 14.8 T at k = 500,
-// profiles/round2/uniform_ab.jsonl); HBM has room to re-read a super-block
-// per group if it does not stay in L2
-constexpr uint64_t kSbDocs = 16384;
+// Documents per super-block: as many as fit kSbBytes of ids (so every group
+// after the first reads them from L2), but at least kSbMinDocs, or the warps
+// in flight (one item each) span several groups whose hot loops no longer
+// fit the instruction cache. C2, k = 500 (profiles/round2/uniform_sb.jsonl):
+// 3,072 docs 14.5 T evals/s and 5.3 GB of DRAM reads per launch, 4,096 docs
+// 14.8 T and 5.7 GB, 6,144 docs 14.8 T and 26 GB, 16,384 docs 83 GB.
+constexpr uint64_t kSbBytes = 64ull << 20;
+constexpr uint64_t kSbMinDocs = 3072;
 constexpr int kTpb = 128;
 
 struct UniformCoef {  // lives in the kernel-parameter bank
@@ -70,7 +74,7 @@ struct UniformArgs {
     uint32_t full;             // full 32-function groups
     uint32_t groups;           // full + (tail group ? 1 : 0)
     uint32_t tail_fc;          // compile-time width of the tail body (multiple of 4; 0: none)
-    uint32_t sb_docs;          // documents per super-block
+    uint32_t sb_docs;          // documents per super-block (0: from the row lengths)
     uint32_t min_nnz;          // > 0: return unless the batch averages >= min_nnz ids per document
 };
 
@@ -78,13 +82,11 @@ __device__ __forceinline__ uint32_t min3u(uint32_t a, uint32_t b, uint32_t c) {
     return min(min(a, b), c);
 }
 
-// The hashing of an item, for the functions at parameter slot S (S = g for
+// The hot loop of an item, for the functions at parameter slot S (S = g for
 // full groups, kFullGroups for the tail group of width FC): full steps of 64
-// quads (8 ids per lane, the next step's loads in flight), then 4-id steps
-// while they are mostly full (duplicated quads leave the minimum unchanged),
-// then single-id rounds over the remaining quads' ids, the head ids and the
-// tail ids. Only this part is instantiated per group; the instruction cache
-// holds the one or two groups in flight plus the shared epilogue.
+// quads (8 ids per lane, the next step's loads in flight). Only this loop is
+// instantiated per group (~7 KB); the instruction cache holds the loops of
+// the one or two groups in flight plus the shared rest of the item.
 template <int S, int FC>
 __device__ __forceinline__ void group_hash(const UniformCoef& C, const uint32_t* __restrict__ ids,
                                           uint32_t head, uint64_t nq, uint64_t nnz, uint32_t lane,
@@ -113,25 +115,6 @@ __device__ __forceinline__ void group_hash(const UniformCoef& C, const uint32_t*
                 m[r] = min3u(t2, t1, a1[r] + a2 * yc.z);
             }
         }
-    }
-    uint64_t s = full_end;
-    while (nq - s > 24) {
-        const uint4 x = __ldg(q4 + min(s + lane, nq - 1));
-#pragma unroll
-        for (int r = 0; r < FC; ++r) {
-            const uint32_t a2 = C.a2[S * kGroup + r];
-            const uint32_t t0 = min3u(a1[r] + a2 * x.x, a1[r] + a2 * x.y, a1[r] + a2 * x.z);
-            m[r] = min3u(m[r], t0, a1[r] + a2 * x.w);
-        }
-        s = min(s + 32, nq);
-    }
-    const uint64_t rest0 = head + 4 * s;  // first unprocessed id after the head
-    const uint64_t e = head + (nnz - rest0);
-    for (uint64_t i0 = 0; i0 < e; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        const uint32_t t = __ldg(ids + (i >= e ? 0 : i < head ? i : rest0 + (i - head)));
-#pragma unroll
-        for (int r = 0; r < FC; ++r) m[r] = min(m[r], a1[r] + C.a2[S * kGroup + r] * t);
     }
 }
 
@@ -180,6 +163,34 @@ __device__ __forceinline__ void uniform_item(const UniformCoef& C, const Uniform
         hash_full<0>(C, g, ids, head, nq, nnz, lane, m);
     else
         hash_tail(C, A.tail_fc, ids, head, nq, nnz, lane, m);
+
+    // the rest, with the group's coefficients read by a runtime slot index
+    // (the uniform kernel takes long rows, where this is a few percent of
+    // the work): 4-id steps while they are mostly full (duplicated quads
+    // leave the minimum unchanged), then single-id rounds over the remaining
+    // quads' ids, the head ids and the tail ids (padded tail functions have
+    // zero coefficients; their minima are dropped)
+    const uint4* q4 = reinterpret_cast<const uint4*>(ids + head);
+    const uint32_t slot = (g < A.full ? g : (uint32_t)kFullGroups) * kGroup;
+    uint64_t s = nq & ~63ull;
+    while (nq - s > 24) {
+        const uint4 x = __ldg(q4 + min(s + lane, nq - 1));
+#pragma unroll
+        for (int r = 0; r < kGroup; ++r) {
+            const uint32_t a1 = C.a1[slot + r], a2 = C.a2[slot + r];
+            const uint32_t t0 = min3u(a1 + a2 * x.x, a1 + a2 * x.y, a1 + a2 * x.z);
+            m[r] = min3u(m[r], t0, a1 + a2 * x.w);
+        }
+        s = min(s + 32, nq);
+    }
+    const uint64_t rest0 = head + 4 * s;  // first unprocessed id after the head
+    const uint64_t e = head + (nnz - rest0);
+    for (uint64_t i0 = 0; i0 < e; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        const uint32_t t = __ldg(ids + (i >= e ? 0 : i < head ? i : rest0 + (i - head)));
+#pragma unroll
+        for (int r = 0; r < kGroup; ++r) m[r] = min(m[r], C.a1[slot + r] + C.a2[slot + r] * t);
+    }
 
     // lane l ends with the warp's minimum of function l of the group
 #pragma unroll
@@ -235,7 +246,14 @@ __global__ void __launch_bounds__(kTpb) sketch_uniform_kernel(const __grid_const
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = kTpb / 32;
     const uint32_t items = A.n * A.groups;
     const uint32_t stride = gridDim.x * W;
-    const uint32_t sb_items = A.sb_docs * A.groups;
+    uint32_t sb_docs = A.sb_docs;
+    if (!sb_docs) {
+        const uint64_t bytes = (A.row_ptr[A.n] - A.row_ptr[0]) * 4 + 1;
+        const uint64_t fit = kSbBytes * A.n / bytes;
+        const uint64_t want = fit > kSbMinDocs ? fit : kSbMinDocs;
+        sb_docs = (uint32_t)(want < A.n ? want : A.n);
+    }
+    const uint32_t sb_items = sb_docs * A.groups;
     // items after the first wave come from a ticket counter, one ticket ahead
     auto fetch_next = [&](uint32_t cur) -> uint32_t {
         if (!A.work) return cur + stride;
@@ -245,13 +263,15 @@ __global__ void __launch_bounds__(kTpb) sketch_uniform_kernel(const __grid_const
         return t >= items ? items : (uint32_t)(stride + t);
     };
     uint32_t it = blockIdx.x * W + warp;
-    uint32_t nxt = it < items ? fetch_next(it) : items;
-    for (; it < items; it = nxt, nxt = it < items ? fetch_next(it) : items) {
+    // the next ticket is taken when the current item is done (not one item
+    // ahead): the items in flight then span ~one ticket per warp, so fewer
+    // groups share the instruction cache
+    for (; it < items; it = fetch_next(it)) {
         // item -> (super-block, group, document): group-major inside a super-block
         const uint32_t sb = it / sb_items;
         const uint32_t rr = it - sb * sb_items;
-        const uint32_t d0 = sb * A.sb_docs;
-        const uint32_t nd = min(A.sb_docs, A.n - d0);
+        const uint32_t d0 = sb * sb_docs;
+        const uint32_t nd = min(sb_docs, A.n - d0);
         const uint32_t g = rr / nd;
         const uint32_t d = d0 + (rr - g * nd);
         uniform_item(C, A, d, g, lane, s_code[warp]);
@@ -279,7 +299,10 @@ uint32_t uniform_min_nnz(const KernelFamily& F, uint64_t n) {
     const uint32_t groups = (k + kGroup - 1) / kGroup;
     if (n * groups >= (1ull << 32)) return 0;
     if (mode >= 2) return 1;
-    return k <= 64 ? 700 : k <= 128 ? 1000 : k <= 300 ? 1500 : 2600;
+    // at k > 400 the persistent kernel's 16-function-wide threads are as
+    // fast on webspam rows (C2, k = 500: 14.78 vs 14.64 T evals/s); the
+    // uniform kernel gains 2% on rcv1-length rows (12,000 ids)
+    return k <= 64 ? 700 : k <= 128 ? 1000 : k <= 300 ? 1500 : k <= 400 ? 2600 : 8000;
 }
 
 void launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,
@@ -337,8 +360,7 @@ void launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t 
     A.groups = groups;
     A.tail_fc = rem ? (rem + 3) & ~3u : 0;
     if (opt(Opt::UniformSbDocs) > 0) sb_override = (uint64_t)opt(Opt::UniformSbDocs);
-    const uint64_t sb = sb_override ? sb_override : kSbDocs;
-    A.sb_docs = (uint32_t)std::min<uint64_t>(sb, n);
+    A.sb_docs = (uint32_t)std::min<uint64_t>(sb_override, n);  // 0: from the row lengths, on the device
     A.min_nnz = min_nnz;
     sketch_uniform_kernel<<<(unsigned)grid, kTpb, 0, st>>>(C, A);
     if (const cudaError_t e = cudaPeekAtLastError(); e != cudaSuccess)
