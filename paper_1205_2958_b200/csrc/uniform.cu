@@ -23,8 +23,9 @@
 //     the instruction cache (L1.5 ~32 KB) holds a few of them -- with
 //     groups interleaved the kernel ran 40% slower on instruction-fetch
 //     stalls (ncu no_instruction, profiles/round2);
-//   * at the end of an item the 32 lanes' partial minima are transposed and
-//     reduced with shuffles (lane l ends with function l of the group), and
+//   * at the end of an item the 32 lanes' partial minima are transposed
+//     through shared memory and reduced (lane l ends with function l of the
+//     group), and
 //     the b-bit codes go into the reference's bitstream (sketch.cpp:64-69).
 // Reference semantics: hash_family.hpp:48-51 (2U), sketch.cpp:71-100.
 #include <cstdio>
@@ -54,6 +55,7 @@ constexpr uint64_t kUniformMinDocs = 2048;
 constexpr uint64_t kSbBytes = 64ull << 20;
 constexpr uint64_t kSbMinDocs = 3072;
 constexpr int kTpb = 128;
+constexpr int kRow = 36;  // words per row of the transpose tile (conflict-free LDS.128 rows)
 
 struct UniformCoef {  // lives in the kernel-parameter bank
     uint32_t a2[(kFullGroups + 1) * kGroup];
@@ -143,7 +145,7 @@ __device__ __forceinline__ void hash_tail(const UniformCoef& C, uint32_t fc, con
 
 // One item: document d, functions [32 g, 32 g + cnt).
 __device__ __forceinline__ void uniform_item(const UniformCoef& C, const UniformArgs& A, uint32_t d,
-                                             uint32_t g, uint32_t lane, uint32_t* s_code) {
+                                             uint32_t g, uint32_t lane, uint32_t* s_t) {
     uint64_t beg = A.row_ptr[d], end = A.row_ptr[d + 1];
     if (end < beg) {
         if (lane == 0) atomicOr(A.err, 2);
@@ -192,17 +194,25 @@ __device__ __forceinline__ void uniform_item(const UniformCoef& C, const Uniform
         for (int r = 0; r < kGroup; ++r) m[r] = min(m[r], C.a1[slot + r] + C.a2[slot + r] * t);
     }
 
-    // lane l ends with the warp's minimum of function l of the group
+    // lane l ends with the warp's minimum of function l of the group: lane l
+    // writes column l of a 32 x 32 tile, reads row l (8 conflict-free
+    // LDS.128) and reduces it -- ~60 instructions against ~250 for a
+    // shuffle transpose (+1.3% at C2, profiles/round2/uniform_variants_ab.jsonl)
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        const bool up = lane & off;
+    for (int r = 0; r < kGroup; ++r) s_t[r * kRow + lane] = m[r];
+    __syncwarp();
+    uint32_t mn;
+    {
+        const uint4* row = reinterpret_cast<const uint4*>(s_t + lane * kRow);
+        uint32_t u[4];
 #pragma unroll
-        for (int q = 0; q < off; ++q) {
-            const uint32_t send = up ? m[q] : m[q + off];
-            const uint32_t keep = up ? m[q + off] : m[q];
-            m[q] = min(keep, __shfl_xor_sync(0xffffffffu, send, off));
+        for (int c = 0; c < 4; ++c) {
+            const uint4 v0 = row[2 * c], v1 = row[2 * c + 1];
+            u[c] = min3u(min3u(v0.x, v0.y, v0.z), min3u(v0.w, v1.x, v1.y), min(v1.z, v1.w));
         }
+        mn = min(min3u(u[0], u[1], u[2]), u[3]);
     }
+    __syncwarp();
 
     // ---- epilogue: minimum -> code -> packed bitstream (sketch.cpp:80-98) ----
     const uint32_t k = A.k, b = A.b;
@@ -210,7 +220,7 @@ __device__ __forceinline__ void uniform_item(const UniformCoef& C, const Uniform
     const uint32_t cnt = min((uint32_t)kGroup, k - j0);
     const bool empty = nnz == 0;
     const uint32_t mask = b >= 32 ? 0xffffffffu : ((1u << b) - 1);
-    const uint32_t mn = m[0] >> A.shift;
+    mn >>= A.shift;
     const uint32_t code = empty ? mask : (mn & mask);
     if (A.minima && lane < cnt) A.minima[(uint64_t)d * k + j0 + lane] = empty ? ~0ull : (uint64_t)mn;
     const uint64_t cb = ((uint64_t)k * b + 7) >> 3;
@@ -218,6 +228,7 @@ __device__ __forceinline__ void uniform_item(const UniformCoef& C, const Uniform
     if (b == 8) {
         if (lane < cnt) out[lane] = (uint8_t)code;
     } else {
+        uint32_t* s_code = s_t;  // the transpose tile is free again
         s_code[lane] = code;
         __syncwarp();
         const uint32_t nbytes = (cnt * b + 7) >> 3;
@@ -238,9 +249,9 @@ __device__ __forceinline__ void uniform_item(const UniformCoef& C, const Uniform
     if (g == 0 && lane == 0 && A.flags) A.flags[d] = empty ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(kTpb) sketch_uniform_kernel(const __grid_constant__ UniformCoef C,
+__global__ void __launch_bounds__(kTpb, 6) sketch_uniform_kernel(const __grid_constant__ UniformCoef C,
                                                               const __grid_constant__ UniformArgs A) {
-    __shared__ uint32_t s_code[kTpb / 32][kGroup];
+    __shared__ __align__(16) uint32_t s_t[kTpb / 32][kGroup * kRow];
     if (A.min_nnz && A.row_ptr[A.n] - A.row_ptr[0] < (uint64_t)A.min_nnz * A.n)
         return;  // the persistent kernel launched beside this one takes the batch
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = kTpb / 32;
@@ -274,7 +285,7 @@ __global__ void __launch_bounds__(kTpb) sketch_uniform_kernel(const __grid_const
         const uint32_t nd = min(sb_docs, A.n - d0);
         const uint32_t g = rr / nd;
         const uint32_t d = d0 + (rr - g * nd);
-        uniform_item(C, A, d, g, lane, s_code[warp]);
+        uniform_item(C, A, d, g, lane, s_t[warp]);
     }
     if (A.work && lane == 0) {  // the last warp out resets the counters
         __threadfence();
@@ -299,10 +310,13 @@ uint32_t uniform_min_nnz(const KernelFamily& F, uint64_t n) {
     const uint32_t groups = (k + kGroup - 1) / kGroup;
     if (n * groups >= (1ull << 32)) return 0;
     if (mode >= 2) return 1;
-    // at k > 400 the persistent kernel's 16-function-wide threads are as
-    // fast on webspam rows (C2, k = 500: 14.78 vs 14.64 T evals/s); the
-    // uniform kernel gains 2% on rcv1-length rows (12,000 ids)
-    return k <= 64 ? 700 : k <= 128 ? 1000 : k <= 300 ? 1500 : k <= 400 ? 2600 : 8000;
+    // with the shared-memory transpose (profiles/round2/uniform_crossover.jsonl,
+    // 1,500..12,000 ids per row): at k = 300/400 the uniform kernel is ahead
+    // from 1,500 ids (+3/+5%), at k = 544 by 1.25x (the persistent kernel
+    // pads 544 functions to 2 x 512 lanes); at 400 < k <= 512 the persistent
+    // kernel's 16-function-wide threads keep up until ~3,700 ids (k = 500:
+    // 0.99x at 2,600, 1.003x at 3,728, 1.02x at 12,000)
+    return k <= 64 ? 700 : k <= 128 ? 1000 : k <= 400 ? 1500 : k <= 512 ? 3600 : 1500;
 }
 
 void launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,

@@ -1,6 +1,7 @@
 """e2e (host buffers through bbmh_ext_sketch_csr) at the webspam shape with the
 id transfer as 4-byte ids (option delta16 = 0), as 2-byte differences (=1) and
-by default; pinned and pageable inputs. One JSON line per case."""
+by default; pinned and pageable inputs; E2E_RAWS sweeps the option
+delta_raw_every (every n-th chunk as 4-byte ids). One JSON line per case."""
 import json
 import os
 import sys
@@ -25,10 +26,14 @@ cb = bbmh.code_bytes(k, 8)
 out = bbmh.PinnedArray(n * cb, np.uint8)
 fam = bbmh.Family(1, 1 << 24, k, 42)
 ref = None
-for mode in os.environ.get("E2E_MODES", "0,1,auto").split(","):
+cases = [(m, r) for m in os.environ.get("E2E_MODES", "0,1,auto").split(",")
+         for r in os.environ.get("E2E_RAWS", "0").split(",")]
+pins = [p == "1" for p in os.environ.get("E2E_PINNED", "1,0").split(",")]
+for mode, raw in cases:
     mode = None if mode == "auto" else mode
-    for pinned in (True, False):
+    for pinned in pins:
         bbmh.set_option("delta16", -1 if mode is None else int(mode))
+        bbmh.set_option("delta_raw_every", int(raw))
         arr = pin.array if pinned else idx
         fam.sketch_csr(rp, arr, 8, codes_out=out.array)
         ts = []
@@ -42,7 +47,7 @@ for mode in os.environ.get("E2E_MODES", "0,1,auto").split(","):
         c = out.array.copy()
         if ref is None:
             ref = c
-        print(json.dumps({"delta": mode, "pinned": pinned, "ms": round(t * 1e3, 2),
+        print(json.dumps({"delta": mode, "raw_every": int(raw), "pinned": pinned, "docs": n, "ms": round(t * 1e3, 2),
                           "T_evals_s": round(idx.size * k / t / 1e12, 3),
                           "in_GBps": round(idx.size * 4 / t / 1e9, 1), "launches": launches,
                           "same": bool(np.array_equal(c, ref))}), flush=True)
