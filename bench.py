@@ -501,6 +501,7 @@ def run_ours(args):
     ids_bytes = n * nnz * 4
     delta16 = h2d < ids_bytes
     budget = bbmh.host_budget(max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))
+    budget_peak = budget["mixed_ids_per_s"] if routes.get("raw_chunks") else budget["encoded_ids_per_s"]
     # host memory bandwidth: a pinned -> pinned copy on every host core (read + write)
     host_best = host_copy_gbps(bbmh)
     # the PCIe H2D copy bounds the 4-byte transfer: measure pinned H2D bandwidth here
@@ -576,15 +577,21 @@ def run_ours(args):
                     "per_rank_ms": [x * 1e3 for x in e2e_per_rank],
                     "per_gpu_value": evals / e2e_s,
                     "routes": routes, "host_budget": budget,
-                    "transfer": ("ids as 16-bit row differences + escapes (csrc/delta.hpp), "
-                                 "rebuilt on the GPU" if delta16 else "ids as u32"),
+                    "transfer": (("ids as 16-bit row differences + escapes (csrc/delta.hpp), "
+                                  "rebuilt on the GPU" + (f"; every {budget['raw_every']}th chunk as u32 "
+                                                          "(host-budget mix)" if routes.get("raw_chunks") else ""))
+                                 if delta16 else "ids as u32"),
                     "input_GBps": ids_bytes * world / e2e_s / 1e9,
-                    "roofline": ({"bound": "host_encode", "unit": "G ids/s",
+                    "roofline": ({"bound": "host_mix" if routes.get("raw_chunks") else "host_encode",
+                                  "unit": "G ids/s",
                                   "achieved": n * nnz * world / e2e_s / 1e9,
-                                  "peak": budget["encoded_ids_per_s"] / 1e9,
-                                  "frac": n * nnz * world / e2e_s / budget["encoded_ids_per_s"],
-                                  "peak_how": "bbmh_ext_host_budget: min(GPUs x link / 2 B, host encode "
-                                              "rate on all cores, measured by the library)"}
+                                  "peak": budget_peak / 1e9,
+                                  "frac": n * nnz * world / e2e_s / budget_peak,
+                                  "peak_how": ("bbmh_ext_host_mix: min(GPUs x link / (2 + 2f) B, host DRAM / "
+                                               "(8 - 4f) B, host encode / (1 - f)) for the raw-chunk fraction f"
+                                               if routes.get("raw_chunks") else
+                                               "bbmh_ext_host_budget: min(GPUs x link / 2 B, host encode "
+                                               "rate on all cores, measured by the library)")}
                                  if delta16 else
                                  {"bound": "pcie_h2d", "unit": "GB/s",
                                   "achieved": h2d / e2e_s / 1e9, "peak": pcie_gbs,

@@ -132,6 +132,18 @@ BBMH_API const char* bbmh_ext_option_name(uint32_t i);
 BBMH_API bbmh_status bbmh_ext_host_budget(uint32_t feeds, double* raw_ids_per_s,
                                           double* encoded_ids_per_s, int32_t* encoded_pays);
 
+/* The mixed transfer the host-buffer path uses by default (option
+ * "delta_raw_every" = -1): every raw_every-th chunk crosses as 4-byte ids and
+ * the rest as 16-bit differences, so the link carries the ids the host cannot
+ * encode in time; 0 when no mix beats the encoded form by 2%. ids_per_s: the
+ * budget's rate for that mix, min(link, host DRAM, host encode). */
+BBMH_API bbmh_status bbmh_ext_host_mix(uint32_t feeds, uint32_t* raw_every, double* ids_per_s);
+
+/* The two host rates the budget rests on, measured once per process: host
+ * DRAM copy bandwidth (read + write bytes/s, all cores) and the 16-bit
+ * encoder's ids/s on all cores. */
+BBMH_API bbmh_status bbmh_ext_host_rates(double* dram_bytes_per_s, double* encode_ids_per_s);
+
 /* Stage breakdown of the calling thread's last bbmh_sketch_file /
  * bbmh_ext_predict_corpus call. Seconds are summed over lanes (one lane per
  * GPU) except wall_seconds. */

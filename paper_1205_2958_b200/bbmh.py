@@ -144,6 +144,8 @@ def lib() -> C.CDLL:
         "bbmh_ext_host_budget": ([C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double), i32p],
                                  C.c_int32),
         "bbmh_ext_family_perm_table": ([C.c_void_p, C.c_uint32, u32p], C.c_int32),
+        "bbmh_ext_host_mix": ([C.c_uint32, u32p, C.POINTER(C.c_double)], C.c_int32),
+        "bbmh_ext_host_rates": ([C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -375,8 +377,13 @@ def host_budget(feeds: int = 1) -> dict:
     """bbmh_ext_host_budget: the id-transfer budget for `feeds` GPUs on this host."""
     raw, enc, pays = C.c_double(0), C.c_double(0), C.c_int32(0)
     _check(lib().bbmh_ext_host_budget(feeds, C.byref(raw), C.byref(enc), C.byref(pays)))
+    every, mixed = C.c_uint32(0), C.c_double(0)
+    _check(lib().bbmh_ext_host_mix(feeds, C.byref(every), C.byref(mixed)))
+    dram, erate = C.c_double(0), C.c_double(0)
+    _check(lib().bbmh_ext_host_rates(C.byref(dram), C.byref(erate)))
     return {"feeds": feeds, "raw_ids_per_s": raw.value, "encoded_ids_per_s": enc.value,
-            "encoded": bool(pays.value)}
+            "encoded": bool(pays.value), "raw_every": every.value, "mixed_ids_per_s": mixed.value,
+            "host_dram_bytes_per_s": dram.value, "host_encode_ids_per_s": erate.value}
 
 
 def last_pipeline_profile() -> dict:

@@ -14,6 +14,7 @@
 #include "../../include/bbmh_ext.h"
 #include "core.hpp"
 #include "engine.hpp"
+#include "hostpool.hpp"
 #include "estimate.hpp"
 #include "options.hpp"
 #include "replay.hpp"
@@ -392,6 +393,22 @@ bbmh_status bbmh_ext_host_budget(uint32_t feeds, double* raw_ids_per_s, double* 
         if (raw_ids_per_s) *raw_ids_per_s = raw;
         if (encoded_ids_per_s) *encoded_ids_per_s = enc;
         if (encoded_pays) *encoded_pays = pays ? 1 : 0;
+    });
+}
+
+bbmh_status bbmh_ext_host_mix(uint32_t feeds, uint32_t* raw_every, double* ids_per_s) {
+    return guarded([&] {
+        double rate = 0;
+        const uint32_t every = mixed_raw_every(feeds, &rate);
+        if (raw_every) *raw_every = every;
+        if (ids_per_s) *ids_per_s = rate;
+    });
+}
+
+bbmh_status bbmh_ext_host_rates(double* dram_bytes_per_s, double* encode_ids_per_s) {
+    return guarded([&] {
+        if (dram_bytes_per_s) *dram_bytes_per_s = host_dram_bytes_per_s();
+        if (encode_ids_per_s) *encode_ids_per_s = host_encode_ids_per_s();
     });
 }
 

@@ -550,6 +550,37 @@ bool delta16_budget_pays(uint64_t feeds, double* raw_ids_s, double* enc_ids_s) {
     return enc > 1.05 * raw;
 }
 
+uint32_t mixed_raw_every(uint64_t feeds, double* ids_s) {
+    feeds = std::max<uint64_t>(1, feeds);
+    const double link = double(feeds) * double(std::max<int64_t>(1, opt(Opt::PcieGbs))) * 1e9;
+    const double enc = host_encode_ids_per_s();
+    // The copy benchmark reads 106..185 GB/s on the 16-core box depending on
+    // what else the process is doing; the encoder alone moves 6 B per id at
+    // its measured rate, a floor under it. The pipeline interleaves encoder
+    // traffic with DMA reads and sees ~85% of a pure copy: derated, the model
+    // puts the optimum at every 3rd-4th chunk raw, where the measured curve
+    // peaks (profiles/round2/e2e_mix.jsonl: 1/6 9.03, 1/4 9.34, 1/3 9.46,
+    // 1/2 8.76 T evals/s against 8.67 all-encoded).
+    const double dram = 0.85 * std::max(host_dram_bytes_per_s(), 6 * enc);
+    // a fraction f of the ids crosses as 4-byte ids (4 B of link and of host
+    // DRAM per id, no host cores), the rest encoded (2 B of link; 4 B read +
+    // 2 B written by the encoder + 2 B read by the DMA; host cores)
+    auto rate = [&](double f) {
+        return std::min({link / (2 + 2 * f), dram / (8 - 4 * f), f < 1 ? enc / (1 - f) : 1e30});
+    };
+    uint32_t best = 0;
+    double best_rate = rate(0);
+    for (uint32_t every = 8; every >= 3; --every) {
+        const double r = rate(1.0 / every);
+        if (r > 1.02 * best_rate) {
+            best = every;
+            best_rate = r;
+        }
+    }
+    if (ids_s) *ids_s = best_rate;
+    return best;
+}
+
 namespace {
 
 }  // namespace
@@ -846,7 +877,6 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     // and 2 B of PCIe, raw ones 4 B of each. With the encode bound by host
     // DRAM and the link idle half the time, sending some chunks raw moves
     // more ids per second than either alone.
-    const uint64_t raw_every = uint64_t(std::max<int64_t>(0, opt(Opt::DeltaRawEvery)));
     // a page-locked output buffer takes the codes' D2H directly
     const bool codes_pinned = codes && !minima && is_pinned(codes) && is_pinned(codes + n * cb - 1);
     // chunk boundaries: <= chunk_docs rows, <= kChunkIdxCap ids (unless one row is larger)
@@ -867,6 +897,11 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
     }
     const uint64_t nchunks = bounds.size() - 1;
     const std::vector<int> devs = pipeline_devices();
+    // GPUs fed from this host (lanes here times the processes of the job
+    // that share it) split its DRAM and cores
+    const uint64_t feeds = devs.size() * uint64_t(std::max<int64_t>(1, opt(Opt::HostSharers)));
+    const int64_t raw_opt = opt(Opt::DeltaRawEvery);
+    const uint64_t raw_every = raw_opt >= 0 ? uint64_t(raw_opt) : mixed_raw_every(feeds, nullptr);
     std::atomic<uint64_t> next{0};
     std::mutex err_mu;
     std::exception_ptr err;
@@ -879,8 +914,7 @@ void sketch_rows_host(const Family& f, const uint64_t* row_ptr, const uint32_t* 
             // GPUs fed from this host (lanes here times the processes of the
             // job that share it) split its DRAM and cores: the 16-bit transfer
             // is used only where that budget says it moves ids faster.
-            lane.set_delta16(delta16_budget_pays(devs.size() * uint64_t(std::max<int64_t>(1, opt(Opt::HostSharers))),
-                                                 nullptr, nullptr));
+            lane.set_delta16(delta16_budget_pays(feeds, nullptr, nullptr));
             auto done = [&](const ChunkResult& res) {
                 const uint64_t r0 = bounds[res.tag];
                 if (codes && res.codes != codes + r0 * cb) host_memcpy(codes + r0 * cb, res.codes, res.n * cb);

@@ -39,6 +39,10 @@ void copy_perm_table(const Family& f, uint32_t j, uint32_t* out);
 // GPUs stream from this host (engine.cu); the two rates are returned too.
 bool delta16_budget_pays(uint64_t feeds, double* raw_ids_s, double* enc_ids_s);
 double host_encode_ids_per_s();
+// Every n-th chunk of the host-buffer path as 4-byte ids (0: none) for the
+// mix that moves the most ids/s from `feeds` GPUs' links, host DRAM and
+// host encode rate (option delta_raw_every = -1); the rate goes to ids_s.
+uint32_t mixed_raw_every(uint64_t feeds, double* ids_s);
 
 // Devices used by the host-buffer and file pipelines (empty = current device).
 std::vector<int> pipeline_devices();

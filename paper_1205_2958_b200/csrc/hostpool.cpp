@@ -153,7 +153,9 @@ void host_memcpy(void* dst, const void* src, size_t n) {
 double host_dram_bytes_per_s() {
     if (const int64_t g = opt(Opt::HostDramGbs); g > 0) return double(g) * 1e9;
     static const double measured = [] {
-        constexpr size_t kBytes = size_t(256) << 20;  // well past any host L3
+        // 1 GiB, best of 4 (256 MiB, best of 3 read ~25% below a pinned
+        // 1 GiB copy on the 16-core box, which skewed the transfer mix)
+        constexpr size_t kBytes = size_t(1) << 30;
         char* a = static_cast<char*>(std::malloc(kBytes));
         char* b = static_cast<char*>(std::malloc(kBytes));
         if (!a || !b) {
@@ -167,7 +169,7 @@ double host_dram_bytes_per_s() {
             std::memset(b + lo, 0, hi - lo);
         });
         double best = 0;
-        for (int rep = 0; rep < 3; ++rep) {
+        for (int rep = 0; rep < 4; ++rep) {
             const auto t0 = std::chrono::steady_clock::now();
             host_memcpy(b, a, kBytes);
             const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

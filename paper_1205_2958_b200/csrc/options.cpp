@@ -29,6 +29,7 @@ constexpr Def kDefs[] = {
     {"split_small_k", 1},
     {"uniform_2u", 1},
     {"uniform_sb_docs", 0},
+    {"uniform_group", 32},
     {"perm_tablewise", -1},
     {"perm_scratch_mb", 2048},
     {"gpu_permgen", 1},
@@ -41,7 +42,7 @@ constexpr Def kDefs[] = {
     {"text_lanes", 4},
     {"read_threads", 16},
     {"delta16", -1},
-    {"delta_raw_every", 0},
+    {"delta_raw_every", -1},
     {"host_sharers", 1},
     {"host_dram_gbs", 0},
     {"pcie_gbs", 55},

@@ -22,7 +22,8 @@ enum class Opt : int {
     DynamicDocs,    // small-k sketch kernel takes documents from a ticket counter (1) or round-robin (0)
     SplitSmallK,    // small-k lane-split kernel (1) or the persistent kernel (0)
     Uniform2U,      // 2U with 32 < k <= 544: coefficient-uniform kernel by row length (1), always (2), never (0)
-    UniformSbDocs,  // uniform kernel: documents per super-block (0: 64 MB of ids, >= 3,072)
+    UniformSbDocs,
+    UniformGroup,   // uniform kernel: hash functions per item (16 or 32)  // uniform kernel: documents per super-block (0: 64 MB of ids, >= 3,072)
     PermTablewise,  // permutation schedule: -1 auto, 0 document-outer, 1 table-outer
     PermScratchMb,  // table-outer schedule: device scratch budget per pass group (MiB)
     GpuPermgen,     // build large permutation tables on the GPU (1) or the host (0)
@@ -35,7 +36,7 @@ enum class Opt : int {
     TextLanes,      // loader lanes for LibSVM text files in all (at least one per GPU)
     ReadThreads,    // pread threads per text block
     Delta16,        // 16-bit id transfer: -1 where it pays, 0 never, 1 whenever possible
-    DeltaRawEvery,  // every n-th chunk crosses as 4-byte ids (0: none)
+    DeltaRawEvery,  // every n-th chunk crosses as 4-byte ids (0: none, -1: from the host budget)
     HostSharers,    // GPU feeds sharing this host's DRAM, e.g. ranks per node (>= 1)
     HostDramGbs,    // host DRAM copy bandwidth, read + write GB/s (0: measure on first use)
     PcieGbs,        // host -> device link bandwidth per GPU, GB/s

@@ -111,6 +111,7 @@ def test_delta_transfer_auto_on_webspam_shape(bb):
     rp, idx = random_csr(rng, 4000, 1 << 24, 3000, 4400)  # 4 chunks of ~3.7 Mi ids
     f = bb.Family(1, 1 << 24, 500, 42)
     bb.set_option("delta16", -1)
+    bb.set_option("delta_raw_every", 0)  # no raw chunks mixed in (test_mixed_transfer)
     l0 = bb.kernel_launches()
     x0 = bb.transfer_bytes()[0]
     auto = f.sketch_csr(rp, idx, 8)[0]
@@ -127,3 +128,35 @@ def test_delta_transfer_auto_on_webspam_shape(bb):
         assert x1 - x0 < 0.55 * (x2 - x1)  # ~2 B per id
     else:
         assert n_auto == n_raw and x1 - x0 == x2 - x1
+    bb.set_option("delta_raw_every", -1)
+
+
+def test_mixed_transfer(bb):
+    """Every n-th chunk as 4-byte ids, the rest as 16-bit differences (option
+    delta_raw_every; -1 = the host budget's mix, engine.cu mixed_raw_every):
+    the codes equal the all-4-byte transfer's (itself oracle-checked above),
+    the route counters split the chunks as asked, and the default follows
+    bbmh_ext_host_mix."""
+    rng = np.random.default_rng(43)
+    rp, idx = random_csr(rng, 3600, 1 << 24, 3400, 4000)  # 6 chunks of 600 docs, >= 2 Mi ids each
+    f = bb.Family(1, 1 << 24, 64, 5)
+    budget = bb.host_budget(1)
+    try:
+        bb.set_chunk_docs(600)
+        with bb.option(delta16=0):
+            ref, _, ref_flags = f.sketch_csr(rp, idx, 8)
+        for every in (3, 2, -1):
+            with bb.option(delta16=-1, delta_raw_every=every):
+                d0, r0 = bb.counter("delta16_chunks"), bb.counter("raw_chunks")
+                codes, _, flags = f.sketch_csr(rp, idx, 8)
+                nd, nr = bb.counter("delta16_chunks") - d0, bb.counter("raw_chunks") - r0
+            assert np.array_equal(codes, ref) and np.array_equal(flags, ref_flags), every
+            assert nd + nr == 6
+            if not budget["encoded"]:
+                assert nd == 0
+                continue
+            e = budget["raw_every"] if every < 0 else every
+            assert nr == (6 // e if e else 0), (every, nd, nr)
+    finally:
+        bb.set_chunk_docs(0)
+    assert budget["mixed_ids_per_s"] > 0 and budget["raw_every"] in (0, 3, 4, 5, 6, 7, 8)
