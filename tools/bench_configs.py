@@ -12,7 +12,7 @@ Prints one JSON object per line (and writes them to --out):
           b in 1..16, latency p50/p99 through bbmh_ext_sketch_csr
   loader  bbmh_sketch_file on BBCV and LibSVM text corpora: MB/s and the
           read/compute/write split
-  ksweep  which roofline (integer pipes or HBM) binds at k = 1, 8, 32, 200, 500
+  ksweep  which roofline (integer pipes or HBM) binds at k = 1, 8, 32, 64, 200, 300, 500
 Usage: python tools/bench_configs.py [--only c1,c3,...] [--out file.jsonl]
 """
 from __future__ import annotations
@@ -137,7 +137,7 @@ def run_c3(n_docs):
 
 
 def run_ksweep(n_docs):
-    """Which roofline binds at k in {1, 8, 32, 200, 500}: kernel
+    """Which roofline binds at k in {1, 8, 32, 64, 200, 300, 500}: kernel
     throughput on the HBM-resident webspam-shaped corpus, the integer-pipe
     fraction (measured pipe rates, 1,965 MHz) and the HBM fraction of the
     algorithmic bytes (ids in, codes + flags out) per launch."""
@@ -145,7 +145,7 @@ def run_ksweep(n_docs):
     d_rp, d_idx = bench.make_corpus_device(torch, n_docs, bench.NNZ, bench.D_WEBSPAM, 5, dev)
     b = 8
     for scheme, sid, dim in (("2u", 1, 1 << 24), ("4u-bit", 3, bench.D_WEBSPAM)):
-        for k in (1, 8, 32, 200, 500):
+        for k in (1, 8, 32, 64, 200, 300, 500):
             cb = (k * b + 7) // 8
             d_codes = torch.empty(n_docs * cb, dtype=torch.uint8, device=dev)
             d_flags = torch.empty(n_docs, dtype=torch.uint8, device=dev)

@@ -5,7 +5,8 @@ spanning several CTAs, rows longer than one shared-memory tile, empty rows),
 the file pipeline on BBCV and on LibSVM text (GPU parser + CPU fallback),
 the 2-byte id transfer, expansion to BBCV and LibSVM text, fused scoring,
 predict on a BBMH file, all-pairs match counts, the VW projection, the small-k
-kernel with document tickets, range-sharded LibSVM loading and epoch replay.
+kernel with document tickets, the coefficient-uniform 2U kernel, range-sharded
+LibSVM loading and epoch replay.
 No torch; ctypes only. Usage: compute-sanitizer --tool memcheck python
 tools/sanitize_driver.py"""
 import ctypes as C
@@ -34,6 +35,16 @@ def main():
             f.sketch_csr(long_rp, long_idx, 5)
             f.sketch_set(idx[: int(rp[1])], 3)
             f.sketch_score_csr(rp, idx, 4, rng.standard_normal(k << 4))
+    # the coefficient-uniform 2U kernel (uniform.cu): >= 2,048 documents, a
+    # tail group (k = 70), unaligned rows (head/tail ids), empty rows, b = 5
+    # (bitstream packer) and b = 8, minima; k = 544 (every parameter slot)
+    urp, uidx = random_csr(rng, 2100, 1 << 20, 0, 90, empty_every=7)
+    bbmh.set_option("uniform_2u", 2)
+    for k in (70, 544):
+        with bbmh.Family(1, 1 << 20, k, 42) as f:
+            f.sketch_csr(urp, uidx, 5, want_minima=True)
+            f.sketch_csr(urp, uidx, 8)
+    bbmh.set_option("uniform_2u", 1)
     # ids through the 2-byte transfer (delta.cu): escapes, empty rows, a long row
     bbmh.set_option("delta16", 1)
     with bbmh.Family(1, 1 << 20, 70, 42) as f:

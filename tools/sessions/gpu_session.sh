@@ -1,6 +1,6 @@
 #!/bin/bash
 # One gpurun session: tests, smoke, int peaks, bench, launch list, one full ncu capture.
-# Usage (from the repo root, on the GPU box): bash tools/gpu_session.sh [tag]
+# Usage (from the repo root, on the GPU box): bash tools/sessions/gpu_session.sh [tag]
 TAG=${1:-r01}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
