@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden,-Wall",
           "-I" + os.path.join(HERE, "..", "include")]
-SOURCES = ["kernels.cu", "uniform.cu", "delta.cu", "parse.cu", "perm.cu", "permgen.cu", "score.cu", "predict.cu", "match.cu", "vw.cu", "engine.cu", "expand.cu", "replay.cu", "estimate.cpp", "delta.cpp", "hostpool.cpp", "family.cpp", "options.cpp", "io.cpp", "pipeline.cpp",
+SOURCES = ["kernels.cu", "uniform.cu", "uniform4.cu", "delta.cu", "parse.cu", "perm.cu", "permgen.cu", "score.cu", "predict.cu", "match.cu", "vw.cu", "engine.cu", "expand.cu", "replay.cu", "estimate.cpp", "delta.cpp", "hostpool.cpp", "family.cpp", "options.cpp", "io.cpp", "pipeline.cpp",
            "capi.cpp"]
 
 

@@ -180,6 +180,10 @@ std::unique_ptr<DeviceFamily> upload_family(const Family& f, int device,
                              cudaMemcpyHostToDevice));
         kf.coef = df->d_coef;
         if (scheme == Scheme::TwoU) kf.host2u = f.twou.data();  // lives as long as f (and df)
+        if (scheme == Scheme::FourUBit) {
+            df->host_coef = coef;
+            kf.host4u = df->host_coef.data();
+        }
     }
     if (f.scheme == Scheme::Permutation) {
         const size_t bytes = size_t(f.dim) * f.k * sizeof(uint32_t);

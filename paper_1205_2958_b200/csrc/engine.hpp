@@ -21,6 +21,7 @@ struct DeviceFamily {
     int device = -1;
     uint32_t* d_coef = nullptr;
     uint32_t* d_perm = nullptr;
+    std::vector<uint32_t> host_coef;  // the host copy of d_coef (uniform-kernel parameters)
     KernelFamily kf;
     ~DeviceFamily();
 };

@@ -461,6 +461,8 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
                                                            uint8_t* __restrict__ flags, int* err,
                                                            unsigned long long* work) {
     __shared__ uint32_t s_code[4][J];
+    if (Fm.yield_nnz && row_ptr[n_docs] - row_ptr[0] >= (uint64_t)Fm.yield_nnz * n_docs)
+        return;  // the uniform kernel launched beside this one takes the batch
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
     const uint32_t k = Fm.k;
     Coef<SCHEME> c[J];
@@ -587,7 +589,7 @@ __global__ void __launch_bounds__(128) sketch_split_kernel(KernelFamily Fm,
 // of zeroed {ticket, exit} pairs per device, taken round-robin per launch;
 // each launch leaves its pair zeroed, and a pair is reused only 1,023
 // launches later.
-unsigned long long* work_slot(int dev) {
+unsigned long long* work_slot(int dev, int pairs = 1) {
     constexpr int kSlots = 1024;
     static std::mutex mu;
     static std::map<int, unsigned long long*> pools;
@@ -607,7 +609,10 @@ unsigned long long* work_slot(int dev) {
         }
         pool = it->second;
     }
-    return pool + 2 * (seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+    // `pairs` consecutive pairs, not wrapping past the end of the pool
+    uint64_t at = seq.fetch_add(pairs, std::memory_order_relaxed) % kSlots;
+    if (at + pairs > kSlots) at = 0;
+    return pool + 2 * at;
 }
 
 template <int SCHEME, bool POW2, int J, bool TRACE = false>
@@ -758,6 +763,7 @@ void dispatch_split(const KernelFamily& F, const uint64_t* row_ptr, uint64_t bas
 
 int sm_count() { return device_sms(); }
 unsigned long long* ticket_slot(int dev) { return work_slot(dev); }
+unsigned long long* ticket_block(int dev, int pairs) { return work_slot(dev, pairs); }
 
 LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     // Each thread owns J hash functions and streams every staged id, so its
@@ -823,9 +829,22 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
                    uint8_t* flags, int* err, cudaStream_t st, double avg_nnz) {
     if (n == 0) return;
     const uint32_t split_max = F.scheme == S_2U ? 32u : 16u;  // functions a lane holds in registers
-    if (F.k <= split_max && F.scheme != S_PERM && opt(Opt::SplitSmallK)) {
+    // 2U at 16 < k < 32: the coefficient-uniform kernel when the rows are
+    // long enough (uniform.cu), the lane-split kernel otherwise; with device
+    // row_ptr both are launched and the batch's mean row length on the
+    // device decides which one returns at once
+    const uint32_t need_small = F.scheme == S_2U && F.k <= split_max ? uniform_min_nnz(F, n) : 0;
+    const bool uniform_small = need_small && avg_nnz >= need_small;
+    if (F.k <= split_max && F.scheme != S_PERM && opt(Opt::SplitSmallK) && !uniform_small) {
         switch (F.scheme) {
-            case S_2U: return dispatch_split<S_2U, true>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+            case S_2U:
+                if (need_small && avg_nnz < 0) {
+                    launch_uniform_2u(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st, need_small);
+                    KernelFamily Fy = F;
+                    Fy.yield_nnz = need_small;
+                    return dispatch_split<S_2U, true>(Fy, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
+                }
+                return dispatch_split<S_2U, true>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             case S_4UBIT:
                 if (F.dim_pow2)
                     return dispatch_split<S_4UBIT, true>(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
@@ -853,6 +872,8 @@ void launch_sketch(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base
             return dispatch_j<S_2U, true>(Fy, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
         }
         case S_4UBIT:
+            if (uniform4_applies(F, n))
+                return launch_uniform_4u(F, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             if (F.dim_pow2)
                 return dispatch_j<S_4UBIT, true>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);
             return dispatch_j<S_4UBIT, false>(F, sh, row_ptr, base, idx, n, b, codes, minima, flags, err, st);

@@ -26,6 +26,7 @@ struct KernelFamily {
     const uint32_t* coef = nullptr;  // 2U: k*{a1,a2}; 4U-bit: k*{a3,2a2,2a1,2a0}; 4U-mod: k*{a3,a2,a1,a0}
     const uint32_t* perm = nullptr;  // permutation tables, k*dim
     const uint32_t* host2u = nullptr;  // 2U: the family's host k*{a1,a2} (uniform kernel parameters)
+    const uint32_t* host4u = nullptr;  // 4U-bit: the host copy of coef (uniform4 kernel parameters)
     // set per launch: the persistent sketch kernel returns at once when the
     // batch averages >= yield_nnz ids per document (the uniform kernel,
     // launched beside it, takes such batches; see launch_sketch)
@@ -70,7 +71,7 @@ void launch_score(const uint8_t* codes, const uint8_t* flags, uint64_t n, uint32
                   const double* w, uint64_t wdim, double* scores, unsigned long long* bad,
                   cudaStream_t stream);
 
-// The coefficient-uniform 2U kernel (uniform.cu) for 32 < k <= 544 over
+// The coefficient-uniform 2U kernel (uniform.cu) for 16 < k <= 544 over
 // >= 2,048 documents. uniform_min_nnz: the average row length from which it
 // beats the persistent kernel for this batch (0: it does not apply).
 // launch_uniform_2u with min_nnz > 0 returns on the device when the batch
@@ -81,10 +82,19 @@ void launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t 
                        uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream,
                        uint32_t min_nnz);
 
+// The coefficient-uniform 4U-bit kernel (uniform4.cu) for 16 < k <= 1024
+// over >= 2,048 documents.
+bool uniform4_applies(const KernelFamily& F, uint64_t n);
+void launch_uniform_4u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t index_base,
+                       const uint32_t* indices, uint64_t n, uint32_t b, uint8_t* codes,
+                       uint64_t* minima, uint8_t* flags, int* err, cudaStream_t stream);
+
 // SM count of the current device (cached) and a zeroed {ticket, exit}
 // counter pair for one launch (nullptr: none could be allocated).
 int sm_count();
 unsigned long long* ticket_slot(int dev);
+// `pairs` consecutive zeroed pairs (2 x pairs counters); the launch leaves them zeroed
+unsigned long long* ticket_block(int dev, int pairs);
 
 uint64_t kernel_launch_count();
 void count_launches(uint64_t n);

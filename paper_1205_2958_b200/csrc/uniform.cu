@@ -306,7 +306,13 @@ uint32_t uniform_min_nnz(const KernelFamily& F, uint64_t n) {
     const int64_t mode = opt(Opt::Uniform2U);  // 0 off, 1 by row length, 2 whenever it applies
     const uint32_t k = F.k;
     if (F.scheme != 1 || !F.host2u || mode == 0) return 0;
-    if (k <= kGroup || k > kUniformMaxK || n < kUniformMinDocs) return 0;
+    if (k <= 16 || k > kUniformMaxK || n < kUniformMinDocs) return 0;
+    // at k = 32 the lane-split kernel (all functions per lane) is as fast on
+    // webspam rows and 6% faster on 12,000-id rows; at 16 < k < 32 it pays
+    // for functions its lanes hold but the group width does not
+    // (profiles/round2/uniform_smallk_ab.jsonl: k = 20 / 24 / 28 1.55 /
+    // 1.32 / 1.16x at 3,728 ids)
+    if (k == kGroup && mode < 2) return 0;
     const uint32_t groups = (k + kGroup - 1) / kGroup;
     if (n * groups >= (1ull << 32)) return 0;
     if (mode >= 2) return 1;
@@ -316,7 +322,7 @@ uint32_t uniform_min_nnz(const KernelFamily& F, uint64_t n) {
     // pads 544 functions to 2 x 512 lanes); at 400 < k <= 512 the persistent
     // kernel's 16-function-wide threads keep up until ~3,700 ids (k = 500:
     // 0.99x at 2,600, 1.003x at 3,728, 1.02x at 12,000)
-    return k <= 64 ? 700 : k <= 128 ? 1000 : k <= 400 ? 1500 : k <= 512 ? 3600 : 1500;
+    return k < kGroup ? 1500 : k <= 64 ? 700 : k <= 128 ? 1000 : k <= 400 ? 1500 : k <= 512 ? 3600 : 1500;
 }
 
 void launch_uniform_2u(const KernelFamily& F, const uint64_t* row_ptr, uint64_t base,

@@ -1,10 +1,11 @@
 """GPU parity of the coefficient-uniform 2U kernel (csrc/uniform.cu).
 
-2U batches with 32 < k <= 544 over >= 2,048 documents run a kernel in which
+2U batches with 16 < k <= 544 over >= 2,048 documents run a kernel in which
 a warp takes one (document, group of 32 functions) item, lanes take
 different ids and the group's coefficients are kernel parameters. Its edges:
-k around the 32-function group size and the tail-group widths, the largest
-k it takes (544) and the first it does not (545), rows shorter than one
+k around the 32-function group size and the tail-group widths (a single
+tail group for 16 < k < 32), the largest k it takes (544) and the first it
+does not (545, and 16 below), rows shorter than one
 hot-loop step (256 ids), rows with misaligned starts and 1-3 tail ids,
 empty rows, every b, minima and flags. Each case is checked against the
 pinned oracle and proven to have taken the kernel (uniform_launches), and
@@ -33,7 +34,7 @@ def _ragged(rng, n, dim):
     return row_ptr, np.concatenate(rows).astype(np.uint32)
 
 
-@pytest.mark.parametrize("k", [33, 36, 63, 64, 65, 100, 200, 255, 480, 500, 512, 544, 545])
+@pytest.mark.parametrize("k", [16, 17, 20, 31, 32, 33, 36, 63, 64, 65, 100, 200, 255, 480, 500, 512, 544, 545])
 def test_uniform_matches_oracle(bb, port, k):
     rng = np.random.default_rng(1000 + k)
     dim = 1 << 24
@@ -46,7 +47,7 @@ def test_uniform_matches_oracle(bb, port, k):
     u0 = bb.counter("uniform_launches")
     codes, minima, flags = f.sketch_csr(rp, idx, b, want_minima=True)
     took = bb.counter("uniform_launches") - u0
-    assert took >= 1 if k <= 544 else took == 0, (k, took)
+    assert took >= 1 if 16 < k <= 544 else took == 0, (k, took)
     st, h = port.family(1, dim, k, seed, 0, 1 << 30)
     assert st == 0
     s, c2, m2, f2 = port.sketch_csr(h, k, rp, idx, b)
@@ -153,3 +154,37 @@ def test_short_rows_on_device_take_the_persistent_kernel(bb):
         outs.append(codes.cpu())
     bb.set_option("uniform_2u", 1)
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("mean_len", [100, 3700])
+def test_small_k_on_device_both_kernels(bb, mean_len):
+    """2U k = 24 on a device batch: the uniform and lane-split kernels are both
+    launched and the batch's mean row length picks one on the device (long
+    rows: uniform; short rows: lane-split); codes, minima and flags equal the
+    lane-split kernel's alone (uniform_2u = 0)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n, k, b = 2500, 24, 6
+    g = torch.Generator(device=dev)
+    g.manual_seed(mean_len)
+    lens = torch.randint(0, 2 * mean_len, (n,), generator=g, device=dev)
+    rp = torch.full((n + 1,), 1, dtype=torch.int64, device=dev)
+    rp[1:] += torch.cumsum(lens, 0)
+    ids = torch.randint(0, 1 << 24, (int(rp[-1].item()) + 16,), generator=g, device=dev,
+                        dtype=torch.int64).to(torch.int32)
+    f = bb.Family(1, 1 << 24, k, 77)
+    outs = []
+    for mode in (1, 0):
+        bb.set_option("uniform_2u", mode)
+        codes = torch.zeros(n * ((k * b + 7) // 8), dtype=torch.uint8, device=dev)
+        mins = torch.zeros(n * k, dtype=torch.int64, device=dev)
+        flags = torch.zeros(n, dtype=torch.uint8, device=dev)
+        u0 = bb.counter("uniform_launches")
+        f.sketch_csr_device(rp.data_ptr(), ids.data_ptr(), n, b, codes.data_ptr(), mins.data_ptr(),
+                            flags.data_ptr(), index_base=0)
+        torch.cuda.synchronize()
+        assert (bb.counter("uniform_launches") - u0) == (1 if mode == 1 else 0)
+        outs.append((codes.cpu(), mins.cpu(), flags.cpu()))
+    bb.set_option("uniform_2u", 1)
+    for a, c in zip(outs[0], outs[1]):
+        assert torch.equal(a, c)

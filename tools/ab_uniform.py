@@ -3,7 +3,9 @@
 (uniform.cu) on the same HBM-resident webspam-shaped corpus. Every arm's
 codes and minima must equal the persistent kernel's; prints ms and T evals/s
 per (k, b, arm). Developer tool. AB_DOCS, AB_KS ("500,200,..."), AB_BS,
-AB_REPS, AB_NNZ, AB_ARMS (JSON list of option dicts; default: uniform on)."""
+AB_REPS, AB_NNZ, AB_ARMS (JSON list of option dicts; default: uniform on),
+AB_SCHEME ("2u" or "4u-bit": the 4U arms switch uniform_4u; the first arm is
+then uniform_4u = 0)."""
 import json
 import os
 import sys
@@ -15,7 +17,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_1205_2958_b200 import bbmh  # noqa: E402
 
-DEFAULTS = {"uniform_2u": 2, "uniform_sb_docs": 0}
+DEFAULTS = {"uniform_2u": 2, "uniform_sb_docs": 0, "uniform_4u": 2}
 
 
 def main():
@@ -24,13 +26,18 @@ def main():
     ks = [int(x) for x in os.environ.get("AB_KS", "500").split(",")]
     bs = [int(x) for x in os.environ.get("AB_BS", "8").split(",")]
     reps = int(os.environ.get("AB_REPS", "5"))
-    dim = int(os.environ.get("AB_DIM", bench.D_2U))
-    arms = [{"uniform_2u": 0}] + json.loads(os.environ.get("AB_ARMS", "[{\"uniform_2u\": 2}]"))
+    scheme = os.environ.get("AB_SCHEME", "2u")
+    sid, sdim = bench.SCHEMES[scheme]
+    dim = int(os.environ.get("AB_DIM", sdim))
+    if scheme == "2u":
+        arms = [{"uniform_2u": 0}] + json.loads(os.environ.get("AB_ARMS", "[{\"uniform_2u\": 2}]"))
+    else:
+        arms = [{"uniform_4u": 0}] + json.loads(os.environ.get("AB_ARMS", "[{\"uniform_4u\": 2}]"))
     dev = torch.device("cuda", 0)
     d_rp, d_idx = bench.make_corpus_device(torch, n, nnz, dim, 1, dev)
     st = torch.cuda.current_stream()
     for k in ks:
-        fam = bbmh.Family(1, dim, k, bench.SEED)
+        fam = bbmh.Family(sid, dim, k, bench.SEED)
         for b in bs:
             cb = (k * b + 7) // 8
             base = None
@@ -56,7 +63,7 @@ def main():
                 e1.record(st)
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / reps
-                row = {"k": k, "b": b, "arm": arm, "docs": n, "nnz": nnz, "ms": round(ms, 3),
+                row = {"scheme": scheme, "k": k, "b": b, "arm": arm, "docs": n, "nnz": nnz, "ms": round(ms, 3),
                        "tevals": round(n * nnz * k / ms / 1e9, 3)}
                 if base is None:
                     base = (ms, got)

@@ -145,7 +145,7 @@ def run_ksweep(n_docs):
     d_rp, d_idx = bench.make_corpus_device(torch, n_docs, bench.NNZ, bench.D_WEBSPAM, 5, dev)
     b = 8
     for scheme, sid, dim in (("2u", 1, 1 << 24), ("4u-bit", 3, bench.D_WEBSPAM)):
-        for k in (1, 8, 32, 64, 200, 300, 500):
+        for k in (1, 8, 24, 32, 64, 200, 300, 500):
             cb = (k * b + 7) // 8
             d_codes = torch.empty(n_docs * cb, dtype=torch.uint8, device=dev)
             d_flags = torch.empty(n_docs, dtype=torch.uint8, device=dev)

@@ -5,7 +5,7 @@ spanning several CTAs, rows longer than one shared-memory tile, empty rows),
 the file pipeline on BBCV and on LibSVM text (GPU parser + CPU fallback),
 the 2-byte id transfer, expansion to BBCV and LibSVM text, fused scoring,
 predict on a BBMH file, all-pairs match counts, the VW projection, the small-k
-kernel with document tickets, the coefficient-uniform 2U kernel, range-sharded
+kernel with document tickets, the coefficient-uniform 2U and 4U kernels, range-sharded
 LibSVM loading and epoch replay.
 No torch; ctypes only. Usage: compute-sanitizer --tool memcheck python
 tools/sanitize_driver.py"""
@@ -24,7 +24,29 @@ from helpers import bbcv_bytes, random_csr  # noqa: E402
 from paper_1205_2958_b200 import bbmh  # noqa: E402
 
 
+def uniform_part(rng):
+    # the coefficient-uniform 2U kernel (uniform.cu): >= 2,048 documents, a
+    # tail group (k = 70), unaligned rows (head/tail ids), empty rows, b = 5
+    # (bitstream packer) and b = 8, minima (kept small: racecheck instruments
+    # every shared-memory access)
+    urp, uidx = random_csr(rng, 2048, 1 << 20, 0, 12, empty_every=7)
+    bbmh.set_option("uniform_2u", 2)
+    with bbmh.Family(1, 1 << 20, 70, 42) as f:
+        f.sketch_csr(urp, uidx, 5, want_minima=True)
+        f.sketch_csr(urp, uidx, 8)
+    bbmh.set_option("uniform_2u", 1)
+    # the coefficient-uniform 4U-bit kernel (uniform4.cu), general and
+    # power-of-two D
+    bbmh.set_option("uniform_4u", 2)
+    for dim in (1000003, 1 << 20):
+        with bbmh.Family(3, dim, 70, 42) as f:
+            f.sketch_csr(urp, uidx, 5, want_minima=True)
+    bbmh.set_option("uniform_4u", 1)
+
+
 def main():
+    if os.environ.get("SANITIZE_ONLY") == "uniform":  # the uniform kernels alone (racecheck)
+        return uniform_part(np.random.default_rng(1))
     rng = np.random.default_rng(1)
     rp, idx = random_csr(rng, 12, 1 << 20, 0, 700, empty_every=5)
     long_rp, long_idx = random_csr(rng, 2, 1 << 20, 9000, 9000)
@@ -35,16 +57,8 @@ def main():
             f.sketch_csr(long_rp, long_idx, 5)
             f.sketch_set(idx[: int(rp[1])], 3)
             f.sketch_score_csr(rp, idx, 4, rng.standard_normal(k << 4))
-    # the coefficient-uniform 2U kernel (uniform.cu): >= 2,048 documents, a
-    # tail group (k = 70), unaligned rows (head/tail ids), empty rows, b = 5
-    # (bitstream packer) and b = 8, minima; k = 544 (every parameter slot)
-    urp, uidx = random_csr(rng, 2100, 1 << 20, 0, 90, empty_every=7)
-    bbmh.set_option("uniform_2u", 2)
-    for k in (70, 544):
-        with bbmh.Family(1, 1 << 20, k, 42) as f:
-            f.sketch_csr(urp, uidx, 5, want_minima=True)
-            f.sketch_csr(urp, uidx, 8)
-    bbmh.set_option("uniform_2u", 1)
+    if os.environ.get("SANITIZE_ONLY") != "rest":
+        uniform_part(rng)
     # ids through the 2-byte transfer (delta.cu): escapes, empty rows, a long row
     bbmh.set_option("delta16", 1)
     with bbmh.Family(1, 1 << 20, 70, 42) as f:
@@ -88,9 +102,10 @@ def main():
         acc = C.c_double()
         assert lib.bbmh_predict(model.encode(), sk.encode(), os.path.join(td, "s.tsv").encode(),
                                 C.byref(acc)) == 0, bbmh.last_error()
-        lib.bbmh_vw_project_file.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64]
-        assert lib.bbmh_vw_project_file(corpus.encode(), os.path.join(td, "v.txt").encode(),
-                                        1 << 10, 3) == 0, bbmh.last_error()
+        if os.environ.get("SANITIZE_ONLY") != "rest":  # (racecheck: the VW tests, separately)
+            lib.bbmh_vw_project_file.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64]
+            assert lib.bbmh_vw_project_file(corpus.encode(), os.path.join(td, "v.txt").encode(),
+                                            1 << 10, 3) == 0, bbmh.last_error()
     # small-k lane-split kernel with document tickets (2U k = 8, 4U k = 4)
     for scheme, k_small in ((1, 8), (3, 4)):
         with bbmh.Family(scheme, 1 << 20, k_small, 42) as f:
