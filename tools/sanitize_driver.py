@@ -22,6 +22,15 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 from helpers import bbcv_bytes, random_csr  # noqa: E402
 from paper_1205_2958_b200 import bbmh  # noqa: E402
+import time as _time  # noqa: E402
+_T0 = _time.perf_counter()
+
+
+def _mark(what):
+    """progress on stderr with the elapsed time (to see what a slow
+    sanitizer pass is in)"""
+    import time
+    print(f"[{time.perf_counter() - _T0:8.1f}s] {what}", file=sys.stderr, flush=True)
 
 
 def uniform_part(rng):
@@ -47,6 +56,7 @@ def uniform_part(rng):
 def main():
     if os.environ.get("SANITIZE_ONLY") == "uniform":  # the uniform kernels alone (racecheck)
         return uniform_part(np.random.default_rng(1))
+    _mark("sketch, every scheme")
     rng = np.random.default_rng(1)
     rp, idx = random_csr(rng, 12, 1 << 20, 0, 700, empty_every=5)
     long_rp, long_idx = random_csr(rng, 2, 1 << 20, 9000, 9000)
@@ -59,6 +69,7 @@ def main():
             f.sketch_score_csr(rp, idx, 4, rng.standard_normal(k << 4))
     if os.environ.get("SANITIZE_ONLY") != "rest":
         uniform_part(rng)
+    _mark("ids through the 2-byte transfer (delta.c")
     # ids through the 2-byte transfer (delta.cu): escapes, empty rows, a long row
     bbmh.set_option("delta16", 1)
     with bbmh.Family(1, 1 << 20, 70, 42) as f:
@@ -72,10 +83,12 @@ def main():
     bbmh.set_option("perm_tablewise", 0)
     with bbmh.Family(0, 1 << 12, 9, 42) as f:
         f.sketch_csr(rp, idx % (1 << 12), 6)
+    _mark(">= 64 MB of tables: built on the GPU (pe")
     # >= 64 MB of tables: built on the GPU (permgen.cu), read back by map()
     with bbmh.Family(0, 1 << 20, 17, 42, 0, 1 << 30) as f:
         f.sketch_csr(rp, idx, 6)
         assert 0 <= f.map(16, 12345) < (1 << 20)
+    _mark("file pipeline, expansion, score, predict, VW")
     with tempfile.TemporaryDirectory() as td:
         rows = [(1 if i % 2 else -1, idx[int(rp[i]):int(rp[i + 1])]) for i in range(12)]
         corpus = os.path.join(td, "c.bbcv")
@@ -106,6 +119,7 @@ def main():
             lib.bbmh_vw_project_file.argtypes = [C.c_char_p, C.c_char_p, C.c_uint32, C.c_uint64]
             assert lib.bbmh_vw_project_file(corpus.encode(), os.path.join(td, "v.txt").encode(),
                                             1 << 10, 3) == 0, bbmh.last_error()
+    _mark("small-k lane-split kernel with document ")
     # small-k lane-split kernel with document tickets (2U k = 8, 4U k = 4)
     for scheme, k_small in ((1, 8), (3, 4)):
         with bbmh.Family(scheme, 1 << 20, k_small, 42) as f:
@@ -115,6 +129,7 @@ def main():
         txt = os.path.join(td, "c.txt")
         lines = ["%+d" % lab + "".join(" %d:1" % (t + 1) for t in ids) for lab, ids in rows]
         open(txt, "w").write("\n".join(lines * 20) + "\n")
+        _mark("range-sharded LibSVM loading, epoch replay")
         # range-sharded LibSVM loading: two lanes on this device, three ranges each
         bbmh.set_devices([0, 0])
         bbmh.set_option("range_shards", 3)
@@ -130,6 +145,7 @@ def main():
                     while r.next()[0]:
                         pass
                     r.reset()
+    _mark("match counts")
     k, b = 100, 4
     cb = (k * b + 7) // 8
     A = rng.integers(0, 256, (37, cb), dtype=np.uint8)
