@@ -51,8 +51,11 @@ constexpr uint64_t kUniformMinDocs = 2048;
 // in flight (one item each) span several groups whose hot loops no longer
 // fit the instruction cache. C2, k = 500 (profiles/round2/uniform_sb.jsonl):
 // 3,072 docs 14.5 T evals/s and 5.3 GB of DRAM reads per launch, 4,096 docs
-// 14.8 T and 5.7 GB, 6,144 docs 14.8 T and 26 GB, 16,384 docs 83 GB.
-constexpr uint64_t kSbBytes = 64ull << 20;
+// 14.8 T and 5.7 GB, 6,144 docs 14.8 T and 26 GB, 16,384 docs 83 GB; the
+// 64 MB first chosen gave 4,500 docs and 7.4 GB (ncu, full C2 launch): the
+// super-block in flight and the next one's first items no longer fit L2.
+// 58 MB keeps C2 at ~4,080 docs.
+constexpr uint64_t kSbBytes = 58ull << 20;
 constexpr uint64_t kSbMinDocs = 3072;
 constexpr int kTpb = 128;
 constexpr int kRow = 36;  // words per row of the transpose tile (conflict-free LDS.128 rows)

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_1205_2958_b200 import bbmh  # noqa: E402
 
-DEFAULTS = {"uniform_2u": 2, "uniform_sb_docs": 0, "uniform_4u": 2}
+DEFAULTS = {"uniform_2u": 2, "uniform_sb_docs": 0, "uniform_4u": 2, "shape_j": 0, "shape_tpb": 0}
 
 
 def main():
