@@ -148,3 +148,21 @@ def test_codes_out_is_validated(bb):
         for bad in (np.zeros(3, np.uint8), np.zeros(64, np.uint16), np.zeros((2, 64), np.uint8)[:, ::2]):
             with pytest.raises(ValueError):
                 f.sketch_csr(rp, idx, 8, codes_out=bad)
+
+
+def test_host_budget_and_mix_without_gpu(bb):
+    """The id-transfer budget is host arithmetic over two host measurements
+    (DRAM copy bandwidth, 16-bit encode rate): it runs without a GPU. The
+    mix (bbmh_ext_host_mix) sends every n-th chunk raw with n in 3..8, or
+    none, and never predicts less than the all-encoded form's DRAM-bound
+    rate; with the link scaled up (more feeds) encoding stops paying."""
+    one = bb.host_budget(1)
+    assert one["host_dram_bytes_per_s"] > 1e9 and one["host_encode_ids_per_s"] > 1e8
+    assert one["raw_every"] in (0, 3, 4, 5, 6, 7, 8)
+    assert one["mixed_ids_per_s"] > 0
+    dram = 0.85 * max(one["host_dram_bytes_per_s"], 6 * one["host_encode_ids_per_s"])
+    f0 = min(55e9 / 2, dram / 8, one["host_encode_ids_per_s"])
+    assert one["mixed_ids_per_s"] >= f0 * 0.999
+    many = bb.host_budget(64)
+    assert many["raw_ids_per_s"] >= one["raw_ids_per_s"]
+    assert not many["encoded"]
