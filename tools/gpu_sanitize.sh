@@ -7,8 +7,10 @@ timeout 300 python tools/sanitize_driver.py > $OUT/plain.log 2>&1; echo "exit $?
 for tool in memcheck racecheck synccheck initcheck; do
   # racecheck instruments every shared-memory access: the uniform kernels
   # (thousands of documents) and the VW sort run in separate passes
-  only=""; [ $tool = racecheck ] && only=rest
-  SANITIZE_ONLY=$only timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
+  # (and with blocking launches: racecheck serialises kernels across host
+  # threads, and the multi-threaded pipelines stalled under it otherwise)
+  only=""; blocking=0; [ $tool = racecheck ] && only=rest && blocking=1
+  CUDA_LAUNCH_BLOCKING=$blocking SANITIZE_ONLY=$only timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
       python tools/sanitize_driver.py > $OUT/$tool.log 2>&1
   echo "exit $?" >> $OUT/$tool.log
 done
