@@ -135,8 +135,9 @@ BBMH_API bbmh_status bbmh_ext_host_budget(uint32_t feeds, double* raw_ids_per_s,
 /* The mixed transfer the host-buffer path uses by default (option
  * "delta_raw_every" = -1): every raw_every-th chunk crosses as 4-byte ids and
  * the rest as 16-bit differences, so the link carries the ids the host cannot
- * encode in time; 0 when no mix beats the encoded form by 2%. ids_per_s: the
- * budget's rate for that mix, min(link, host DRAM, host encode). */
+ * encode in time. raw_every is 3..8 (near ties go to more raw chunks), or 0
+ * when the encoded form beats every mix by 2%. ids_per_s: the budget's rate
+ * for that mix, min(link, host DRAM, host encode). */
 BBMH_API bbmh_status bbmh_ext_host_mix(uint32_t feeds, uint32_t* raw_every, double* ids_per_s);
 
 /* The two host rates the budget rests on, measured once per process: host

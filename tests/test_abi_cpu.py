@@ -162,7 +162,7 @@ def test_host_budget_and_mix_without_gpu(bb):
     assert one["mixed_ids_per_s"] > 0
     dram = 0.85 * max(one["host_dram_bytes_per_s"], 6 * one["host_encode_ids_per_s"])
     f0 = min(55e9 / 2, dram / 8, one["host_encode_ids_per_s"])
-    assert one["mixed_ids_per_s"] >= f0 * 0.999
+    assert one["mixed_ids_per_s"] >= f0 * 0.98  # (near ties go to more raw chunks)
     many = bb.host_budget(64)
     assert many["raw_ids_per_s"] >= one["raw_ids_per_s"]
     assert not many["encoded"]
