@@ -30,7 +30,6 @@ constexpr Def kDefs[] = {
     {"uniform_2u", 1},
     {"uniform_sb_docs", 0},
     {"uniform_4u", 1},
-    {"uniform_group", 32},
     {"perm_tablewise", -1},
     {"perm_scratch_mb", 2048},
     {"gpu_permgen", 1},

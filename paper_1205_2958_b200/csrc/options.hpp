@@ -21,10 +21,9 @@ enum class Opt : int {
     Carveout,       // shared-memory carveout % for the sketch kernels (-1: driver default)
     DynamicDocs,    // small-k sketch kernel takes documents from a ticket counter (1) or round-robin (0)
     SplitSmallK,    // small-k lane-split kernel (1) or the persistent kernel (0)
-    Uniform2U,      // 2U with 32 < k <= 544: coefficient-uniform kernel by row length (1), always (2), never (0)
-    UniformSbDocs,
-    Uniform4U,      // 4U-bit with 32 < k <= 1024: coefficient-uniform kernel by the persistent shape (1), always (2), never (0)
-    UniformGroup,   // uniform kernel: hash functions per item (16 or 32)  // uniform kernel: documents per super-block (0: 64 MB of ids, >= 3,072)
+    Uniform2U,      // 2U with 16 < k <= 544: coefficient-uniform kernel by row length (1), always (2), never (0)
+    UniformSbDocs,  // uniform kernels: documents per super-block (0: 58 MB of ids, >= 3,072)
+    Uniform4U,      // 4U-bit with 16 < k <= 1024: coefficient-uniform kernel by the persistent shape (1), always (2), never (0)
     PermTablewise,  // permutation schedule: -1 auto, 0 document-outer, 1 table-outer
     PermScratchMb,  // table-outer schedule: device scratch budget per pass group (MiB)
     GpuPermgen,     // build large permutation tables on the GPU (1) or the host (0)
