@@ -777,7 +777,13 @@ LaunchShape choose_shape(uint32_t k, int scheme, uint64_t n, int sms) {
     // cost (idle j >= k lanes included); for small online batches it prefers
     // more, thinner j-tiles so the batch still fills the GPU. Ties prefer
     // fewer CTAs per document.
-    constexpr double kSatThreads = 384;
+    // 4U's fold chains need more resident threads before an SM saturates:
+    // with 384 the model kept small online batches (a few hundred documents
+    // per chunk) on one 512-lane tile per document and half the SMs idle
+    // (C5 4U-bit, 1,024 docs: 1.92 -> 1.62 ms with two 256-lane tiles,
+    // profiles/round2/c5_4u_shapes.jsonl). Large batches fill every SM under
+    // either figure, so their shapes do not change.
+    const double kSatThreads = (scheme == S_4UBIT || scheme == S_4UMOD) ? 1024 : 384;
     const double docs = n ? (double)n : 1e12;
     LaunchShape best;
     double best_cost = 1e300;
